@@ -1,0 +1,118 @@
+/*
+ * cypress_b200.h -- C ABI of the B200-native (sm_100a) GEMM family that
+ * Cypress (arXiv 2504.07004) compiles: D = alpha*A*B + beta*C with fp32
+ * accumulation, batched, dual-GEMM and GEMM + row-reduction.
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX source).
+ *
+ * General contract (all entry points):
+ *  - extern "C", never throw, never allocate device memory, never
+ *    synchronize.  Work is enqueued on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) of the CURRENT device, which must
+ *    own every pointer.  Return is immediate; asynchronous faults surface on
+ *    the stream like any CUDA kernel.
+ *  - Storage is row-major; every leading dimension (ld*) and batch stride
+ *    (stride*) is in ELEMENTS.  A is m x k, B is k x n, C and D are m x n.
+ *    This matches the paper's logical shapes A[M,K], B[K,N], C[M,N]
+ *    (Fig. 6a); the paper fixes no majorness (R5).
+ *  - A, B, B0, B1, C, C0, C1 are read-only (the paper's read privileges,
+ *    P:495).  If beta == 0, C is NOT read and may be NULL (BLAS rule, R4).
+ *    C == D with ldc == ldd (exact alias) is allowed; any other overlap of
+ *    an output with an input or with another output is CY_ERR_INVALID_VALUE.
+ *  - dtype: A, B, C, D share one 16-bit type (cy_dtype_t); accumulation is
+ *    fp32 in tensor memory; the epilogue computes alpha*acc + beta*C in fp32
+ *    and rounds ONCE to the output type with IEEE round-to-nearest-even
+ *    (R3, R7).  Boundary tiles are handled in-kernel (zero-filled loads,
+ *    clipped stores, R8): no element outside [0,m) x [0,n) is written.
+ *  - m == 0 or n == 0 (or batch == 0): CY_OK, nothing launched.
+ *    k == 0: D = beta*C (y = 0), computed by the same kernel.
+ *  - Hardware rules (TMA): every base pointer 16-byte aligned; every ld and
+ *    stride a multiple of 8 elements (16 bytes), else CY_ERR_MISALIGNED.
+ *    There is no fallback path (no CPU, no library GEMM).
+ *  - Requires compute capability 10.0 (B200, sm_100a); otherwise
+ *    CY_ERR_UNSUPPORTED_DEVICE.
+ *  - Thread safety: calls from several host threads on different streams
+ *    are safe; the library keeps only lazily built, mutex-guarded caches
+ *    (kernel attributes, SM count, driver entry point, TMA descriptors).
+ */
+#ifndef CYPRESS_B200_H_
+#define CYPRESS_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CY_OK = 0,
+  CY_ERR_INVALID_VALUE = 1,      /* bad size, ld, NULL, overlap, mode/pointer mismatch */
+  CY_ERR_MISALIGNED = 2,         /* pointer not 16-B aligned or ld/stride not a multiple of 8 */
+  CY_ERR_UNSUPPORTED_DEVICE = 3, /* current device is not compute capability 10.0 */
+  CY_ERR_LAUNCH = 4,             /* cudaGetLastError() after the launch, or descriptor encode failure */
+  CY_ERR_INTERNAL = 5
+} cy_status_t;
+
+typedef enum { CY_F16 = 0, CY_BF16 = 1 } cy_dtype_t;
+
+/* Dual-GEMM output mode (R1):
+ *  CY_DUAL_PAIR: D0 = alpha*A*B0 + beta*C0 and D1 = alpha*A*B1 + beta*C1
+ *                (BASELINE configs[3], the GLU core P:1532)
+ *  CY_DUAL_SUM:  D0 = alpha*(A*B0 + A*B1) + beta*C0  ("A.B1 + A.B2");
+ *                C1 and D1 must be NULL. */
+typedef enum { CY_DUAL_PAIR = 0, CY_DUAL_SUM = 1 } cy_dual_mode_t;
+
+/* GEMM, "C = A x B", tile program clear -> accumulate over
+ * K tiles -> copy out (Fig. 6a), with BLAS alpha/beta (R4). */
+cy_status_t cy_gemm(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha,
+                    const void* A, int64_t lda, const void* B, int64_t ldb, float beta,
+                    const void* C, int64_t ldc, void* D, int64_t ldd, void* stream);
+
+/* Strided batched GEMM: "L independent GEMMs in a single pass".
+ * X_b = X + b*strideX (elements), b < batch; one launch covers all b. */
+cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch,
+                            float alpha, const void* A, int64_t lda, int64_t strideA,
+                            const void* B, int64_t ldb, int64_t strideB, float beta,
+                            const void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
+                            int64_t strideD, void* stream);
+
+/* Dual GEMM: A*B0 and A*B1 in one kernel sharing the A tiles, B0/B1 copies
+ * overlapped in the main loop.  See cy_dual_mode_t. */
+cy_status_t cy_dual_gemm(cy_dtype_t dt, cy_dual_mode_t mode, int64_t m, int64_t n, int64_t k,
+                         float alpha, const void* A, int64_t lda, const void* B0, int64_t ldb0,
+                         const void* B1, int64_t ldb1, float beta, const void* C0, int64_t ldc0,
+                         const void* C1, int64_t ldc1, void* D0, int64_t ldd0, void* D1,
+                         int64_t ldd1, void* stream);
+
+/* GEMM + row reduction: "C = A.B and y(i) = sum_k A(i,k)" in a single kernel,
+ * the reduction done on SIMT warps from the shared-memory A tiles while the
+ * tensor core computes A.B.  y: m floats (fp32, device),
+ * unscaled and independent of B/alpha/beta/C (R2); must not overlap D. */
+cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha,
+                              const void* A, int64_t lda, const void* B, int64_t ldb, float beta,
+                              const void* C, int64_t ldc, void* D, int64_t ldd, float* y,
+                              void* stream);
+
+/* Human-readable status. */
+const char* cy_status_string(cy_status_t s);
+
+/* ---- tuning / introspection (tests, bench) ---------------------------- */
+
+/* Number of compiled kernel configurations (tile shape x CTA-pairing x stages). */
+int cy_num_configs(void);
+/* Describe config `id`: writes cta_group (1|2), tile_m, tile_n, stages. Returns CY_OK or
+ * CY_ERR_INVALID_VALUE. */
+cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int* stages);
+/* Force config `id` for subsequent GEMM / batched / rowreduce calls of this process
+ * (-1 restores the shape heuristic).  Used by config-invariance tests. */
+cy_status_t cy_force_config(int id);
+/* Config id chosen by the most recent successful launch in this process (-1 if none). */
+int cy_last_config(void);
+/* Number of kernel launches this library issued in this process (monotone counter). */
+int64_t cy_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CYPRESS_B200_H_ */

@@ -1,0 +1,193 @@
+"""paper_2504_07004_b200 -- B200-native (sm_100a) implementation of the GEMM family that
+Cypress (arXiv 2504.07004) compiles: D = alpha*A*B + beta*C with fp32 accumulation, batched,
+dual-GEMM and GEMM + row reduction.
+
+Thin Python binding over the C ABI in ``include/cypress_b200.h`` (``libcypress_b200.so``):
+argument marshalling only -- every arithmetic step runs in the sm_100a kernels.  PyTorch is
+used for device memory and streams.  There is no CPU / library fallback: a missing extension
+raises.
+
+Entry points (same names as the C ABI, plus torch conveniences):
+  gemm(A, B, C=None, alpha=1, beta=0, out=None)            -> D            cy_gemm
+  gemm_batched(A, B, C=None, alpha=1, beta=0, out=None)    -> D (L,m,n)    cy_gemm_batched
+  dual_gemm(A, B0, B1, C0=None, C1=None, mode="pair", ...) -> (D0, D1) | D cy_dual_gemm
+  gemm_rowreduce(A, B, C=None, alpha=1, beta=0, ...)       -> (D, y)       cy_gemm_rowreduce
+Raw pointer calls: ``paper_2504_07004_b200.cy_gemm(...)`` etc. (ctypes signatures of the header).
+"""
+from __future__ import annotations
+
+from . import _lib
+from ._lib import CY_BF16, CY_DUAL_PAIR, CY_DUAL_SUM, CY_F16, CyError, check
+
+__all__ = [
+    "gemm", "gemm_batched", "dual_gemm", "gemm_rowreduce", "CyError", "force_config", "last_config",
+    "num_configs", "config_info", "launch_count", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
+    "cy_gemm_rowreduce", "CY_F16", "CY_BF16", "CY_DUAL_PAIR", "CY_DUAL_SUM",
+]
+
+
+def __getattr__(name):
+    # raw C-ABI entry points: paper_2504_07004_b200.cy_gemm(...) -> status
+    if name.startswith("cy_") and name in _lib.EXPORTS:
+        return getattr(_lib.load(), name)
+    raise AttributeError(name)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dt(t):
+    torch = _torch()
+    if t.dtype == torch.float16:
+        return CY_F16
+    if t.dtype == torch.bfloat16:
+        return CY_BF16
+    raise TypeError(f"cypress_b200: unsupported dtype {t.dtype} (fp16 / bf16 only)")
+
+
+def _ld(t, name):
+    if t.dim() != 2:
+        raise ValueError(f"{name}: expected a 2-D tensor")
+    if t.stride(1) != 1 and t.size(1) > 1:
+        raise ValueError(f"{name}: rows must be contiguous (row-major, stride(1) == 1)")
+    return t.stride(0) if t.size(0) > 1 else max(t.stride(0), t.size(1))
+
+
+def _empty2d(m, n, like):
+    """Row-major m x n output whose row stride is padded to a multiple of 8 elements."""
+    torch = _torch()
+    ld = (n + 7) // 8 * 8
+    return torch.empty((m, ld), dtype=like.dtype, device=like.device)[:, :n]
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _check_dev(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("cypress_b200: all tensors must be CUDA tensors (no CPU fallback)")
+
+
+def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
+    """D = alpha*A@B + beta*C  (A: m x k, B: k x n, row-major).  cy_gemm."""
+    torch = _torch()
+    _check_dev(A, B, C, out)
+    m, k = A.shape
+    n = B.shape[1]
+    if B.shape[0] != k:
+        raise ValueError("inner dimensions differ")
+    if out is None:
+        out = _empty2d(m, n, A)
+    lib = _lib.load()
+    st = lib.cy_gemm(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
+                     _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n,
+                     _ptr(out), _ld(out, "out"), _stream(stream))
+    check(st, "cy_gemm")
+    return out
+
+
+def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
+    """D[b] = alpha*A[b]@B[b] + beta*C[b] for b < L (3-D tensors, rows contiguous)."""
+    torch = _torch()
+    _check_dev(A, B, C, out)
+    L, m, k = A.shape
+    n = B.shape[2]
+    if out is None:
+        out = torch.empty((L, m, n), dtype=A.dtype, device=A.device)
+
+    def lds(t):
+        if t is None:
+            return n, 0
+        if t.stride(2) != 1:
+            raise ValueError("rows must be contiguous")
+        return t.stride(1), t.stride(0)
+
+    lda, sa = lds(A)
+    ldb, sb = lds(B)
+    ldc, sc = lds(C if beta != 0 else None)
+    ldd, sd = lds(out)
+    st = _lib.load().cy_gemm_batched(_dt(A), m, n, k, L, float(alpha), _ptr(A), lda, sa, _ptr(B), ldb, sb,
+                                     float(beta), _ptr(C) if beta != 0 else None, ldc, sc, _ptr(out), ldd, sd,
+                                     _stream(stream))
+    check(st, "cy_gemm_batched")
+    return out
+
+
+def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0, mode: str = "pair",
+              out0=None, out1=None, stream=None):
+    """mode "pair": (D0, D1) = (alpha*A@B0 + beta*C0, alpha*A@B1 + beta*C1);
+    mode "sum": D = alpha*(A@B0 + A@B1) + beta*C0.  cy_dual_gemm."""
+    torch = _torch()
+    _check_dev(A, B0, B1, C0, C1, out0, out1)
+    m, k = A.shape
+    n = B0.shape[1]
+    pair = mode == "pair"
+    if mode not in ("pair", "sum"):
+        raise ValueError("mode must be 'pair' or 'sum'")
+    if out0 is None:
+        out0 = _empty2d(m, n, A)
+    if pair and out1 is None:
+        out1 = _empty2d(m, n, A)
+    use_c = beta != 0
+    st = _lib.load().cy_dual_gemm(
+        _dt(A), CY_DUAL_PAIR if pair else CY_DUAL_SUM, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
+        _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), float(beta), _ptr(C0) if use_c else None,
+        _ld(C0, "C0") if (use_c and C0 is not None) else n, _ptr(C1) if (use_c and pair) else None,
+        _ld(C1, "C1") if (use_c and pair and C1 is not None) else n, _ptr(out0), _ld(out0, "out0"),
+        _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream))
+    check(st, "cy_dual_gemm")
+    return (out0, out1) if pair else out0
+
+
+def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, y=None, stream=None):
+    """D = alpha*A@B + beta*C and y[i] = sum_k A[i,k] (fp32), one kernel.  cy_gemm_rowreduce."""
+    torch = _torch()
+    _check_dev(A, B, C, out, y)
+    m, k = A.shape
+    n = B.shape[1]
+    if out is None:
+        out = _empty2d(m, n, A)
+    if y is None:
+        y = torch.empty((m,), dtype=torch.float32, device=A.device)
+    st = _lib.load().cy_gemm_rowreduce(
+        _dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
+        _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n, _ptr(out),
+        _ld(out, "out"), _ptr(y), _stream(stream))
+    check(st, "cy_gemm_rowreduce")
+    return out, y
+
+
+def force_config(cfg_id: int):
+    check(_lib.load().cy_force_config(int(cfg_id)), "cy_force_config")
+
+
+def last_config() -> int:
+    return int(_lib.load().cy_last_config())
+
+
+def num_configs() -> int:
+    return int(_lib.load().cy_num_configs())
+
+
+def config_info(cfg_id: int) -> dict:
+    import ctypes
+
+    v = [ctypes.c_int() for _ in range(4)]
+    check(_lib.load().cy_config_info(int(cfg_id), *[ctypes.byref(x) for x in v]), "cy_config_info")
+    return {"cta_group": v[0].value, "tile_m": v[1].value, "tile_n": v[2].value, "stages": v[3].value}
+
+
+def launch_count() -> int:
+    return int(_lib.load().cy_launch_count())

@@ -1,0 +1,465 @@
+// cy_gemm.cu -- host side of the C ABI (include/cypress_b200.h): argument validation, TMA
+// descriptor encoding (cached), config selection, cluster launch.  No torch, no libcuda link
+// (the driver's cuTensorMapEncodeTiled is fetched through cudaGetDriverEntryPoint).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "cy_kernel.cuh"
+#include "cypress_b200.h"
+
+namespace {
+
+using cy::Params;
+
+// ------------------------------------------------------------------------------------------
+// kernel menu
+struct KDesc {
+  int var, dt, cg, bn, stages, threads, smem;
+  const void* fn;
+};
+
+template <int DT, int CG, int BN, int ST, int VAR>
+KDesc kdesc() {
+  using C = cy::Cfg<DT, CG, BN, ST, VAR>;
+  return KDesc{VAR, DT, CG, BN, ST, C::THREADS, C::SMEM_BYTES, (const void*)&cy::cy_sm100_kernel<C>};
+}
+
+// Shapes (cta_group, tile N) offered per variant; the GEMM menu defines the public config ids.
+struct Shape { int cg, bn; };
+constexpr Shape kGemmMenu[] = {{2, 256}, {2, 128}, {1, 256}, {1, 128}, {1, 64}};
+constexpr int kNumGemmCfg = sizeof(kGemmMenu) / sizeof(kGemmMenu[0]);
+
+template <int DT>
+void add_all(std::vector<KDesc>& v) {
+  v.push_back(kdesc<DT, 2, 256, 6, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 2, 128, 8, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 1, 256, 4, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 1, 128, 6, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 1, 64, 8, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 2, 256, 6, cy::V_ROWREDUCE>());
+  v.push_back(kdesc<DT, 2, 128, 8, cy::V_ROWREDUCE>());
+  v.push_back(kdesc<DT, 1, 128, 6, cy::V_ROWREDUCE>());
+  v.push_back(kdesc<DT, 2, 128, 6, cy::V_DUAL_PAIR>());
+  v.push_back(kdesc<DT, 2, 256, 4, cy::V_DUAL_PAIR>());
+  v.push_back(kdesc<DT, 1, 128, 4, cy::V_DUAL_PAIR>());
+  v.push_back(kdesc<DT, 2, 256, 4, cy::V_DUAL_SUM>());
+  v.push_back(kdesc<DT, 2, 128, 6, cy::V_DUAL_SUM>());
+  v.push_back(kdesc<DT, 1, 128, 4, cy::V_DUAL_SUM>());
+}
+
+const std::vector<KDesc>& menu() {
+  static const std::vector<KDesc> v = [] {
+    std::vector<KDesc> r;
+    add_all<0>(r);
+    add_all<1>(r);
+    return r;
+  }();
+  return v;
+}
+
+std::atomic<int> g_forced{-1};
+std::atomic<int> g_last{-1};
+std::atomic<int64_t> g_launches{0};
+
+// ------------------------------------------------------------------------------------------
+// per-device state
+struct DevState {
+  bool init = false;
+  bool ok = false;
+  int sms = 0;
+  std::vector<char> attr_set;  // per menu entry: max dynamic smem attribute applied
+};
+std::mutex g_mu;
+DevState g_dev[64];
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+cy_status_t device_state(int& dev, DevState*& st) {
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CY_ERR_UNSUPPORTED_DEVICE;
+  std::lock_guard<std::mutex> lk(g_mu);
+  st = &g_dev[dev];
+  if (!st->init) {
+    st->init = true;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev);
+    st->ok = (major == 10 && minor == 0);
+    st->attr_set.assign(menu().size(), 0);
+    if (!g_encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cudaGetLastError();
+  }
+  if (!st->ok) return CY_ERR_UNSUPPORTED_DEVICE;
+  if (!g_encode) return CY_ERR_INTERNAL;
+  return CY_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA descriptors (3-D: columns, rows, batch), cached
+struct MapKey {
+  const void* ptr;
+  uint64_t cols, rows, batch, ld, stride;
+  uint32_t box_c, box_r;
+  int dt;
+  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+  uint64_t tick;
+};
+std::mutex g_map_mu;
+std::vector<MapEntry> g_maps;
+uint64_t g_tick = 0;
+
+bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64_t rows, uint64_t batch,
+                uint64_t ld, uint64_t stride, uint32_t box_c, uint32_t box_r) {
+  MapKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.ptr = ptr; key.cols = cols; key.rows = rows; key.batch = batch; key.ld = ld; key.stride = stride;
+  key.box_c = box_c; key.box_r = box_r; key.dt = dt;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    for (auto& e : g_maps)
+      if (e.key == key) {
+        e.tick = ++g_tick;
+        *out = e.map;
+        return true;
+      }
+  }
+  cuuint64_t dims[3] = {cols, rows, batch};
+  cuuint64_t strides[2] = {ld * 2, stride * 2};
+  cuuint32_t box[3] = {box_c, box_r, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult r = g_encode(&m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  *out = m;
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (g_maps.size() < 256) {
+    g_maps.push_back(MapEntry{key, m, ++g_tick});
+  } else {
+    auto lru = std::min_element(g_maps.begin(), g_maps.end(),
+                                [](const MapEntry& a, const MapEntry& b) { return a.tick < b.tick; });
+    *lru = MapEntry{key, m, ++g_tick};
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------------------------------
+// validation helpers
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct Range {
+  uintptr_t lo, hi;  // [lo, hi)
+};
+Range span(const void* p, int64_t rows, int64_t cols, int64_t ld, int64_t batch, int64_t stride, int64_t esz) {
+  if (!p || rows <= 0 || cols <= 0 || batch <= 0) return Range{0, 0};
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(p);
+  const int64_t last = (batch - 1) * stride + (rows - 1) * ld + cols;
+  return Range{lo, lo + static_cast<uintptr_t>(last * esz)};
+}
+bool overlap(Range a, Range b) { return a.lo < a.hi && b.lo < b.hi && a.lo < b.hi && b.lo < a.hi; }
+
+// ------------------------------------------------------------------------------------------
+// config choice: minimise (waves x tile area / efficiency)
+double cfg_cost(int cg, int bn, int64_t m, int64_t n, int64_t L, int sms) {
+  const int64_t bm = 128 * cg;
+  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
+  const int64_t units = sms / cg;
+  const int64_t waves = (tiles + units - 1) / units;
+  // relative per-SM tensor efficiency of each tile shape (shared-memory operand traffic per MMA)
+  double eff = 1.0;
+  if (cg == 2 && bn == 128) eff = 0.93;
+  if (cg == 1 && bn == 256) eff = 0.85;
+  if (cg == 1 && bn == 128) eff = 0.72;
+  if (cg == 1 && bn == 64) eff = 0.45;
+  return static_cast<double>(waves) * static_cast<double>(bm * bn) / cg / eff;
+}
+
+int pick(int var, int dt, int64_t m, int64_t n, int64_t L, int sms) {
+  const auto& mn = menu();
+  int forced = g_forced.load();
+  if (forced >= 0 && forced < kNumGemmCfg) {
+    for (size_t i = 0; i < mn.size(); ++i)
+      if (mn[i].var == var && mn[i].dt == dt && mn[i].cg == kGemmMenu[forced].cg &&
+          mn[i].bn == kGemmMenu[forced].bn)
+        return static_cast<int>(i);
+  }
+  int best = -1;
+  double best_cost = 0;
+  for (size_t i = 0; i < mn.size(); ++i) {
+    if (mn[i].var != var || mn[i].dt != dt) continue;
+    double c = cfg_cost(mn[i].cg, mn[i].bn, m, n, L, sms);
+    if (var == cy::V_DUAL_PAIR && mn[i].bn == 256) c *= 1.04;  // single-buffered accumulators
+    if (best < 0 || c < best_cost) { best = static_cast<int>(i); best_cost = c; }
+  }
+  return best;
+}
+
+// ------------------------------------------------------------------------------------------
+struct Operand {
+  const void* ptr;
+  int64_t ld, stride;
+};
+
+cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, float alpha, Operand A,
+                   Operand B0, Operand B1, float beta, Operand C0, Operand C1, Operand D0, Operand D1, float* y,
+                   void* stream) {
+  int dev;
+  DevState* st;
+  cy_status_t s = device_state(dev, st);
+  if (s != CY_OK) return s;
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX || L > INT32_MAX) return CY_ERR_INVALID_VALUE;
+  const int idx = pick(var, dt, m, n, L, st->sms);
+  if (idx < 0) return CY_ERR_INTERNAL;
+  const KDesc& kd = menu()[idx];
+  const int bm = 128 * kd.cg;
+  const int bn_cta = kd.bn / kd.cg;
+
+  CUtensorMap tA, tB0, tB1, tC0, tC1, tD0, tD1;
+  std::memset(&tA, 0, sizeof(CUtensorMap));
+  tB0 = tB1 = tC0 = tC1 = tD0 = tD1 = tA;
+  auto enc = [&](CUtensorMap* out, Operand o, int64_t rows, int64_t cols, uint32_t bc, uint32_t br) {
+    const int64_t stride = (L > 1) ? o.stride : rows * o.ld;
+    return encode_map(out, dt, o.ptr, (uint64_t)cols, (uint64_t)rows, (uint64_t)L, (uint64_t)o.ld,
+                      (uint64_t)stride, bc, br);
+  };
+  bool ok = true;
+  if (k > 0) {
+    ok = ok && enc(&tA, A, m, k, 64, 128);
+    ok = ok && enc(&tB0, B0, k, n, 64, 64);
+    if (B1.ptr) ok = ok && enc(&tB1, B1, k, n, 64, 64);
+  }
+  const bool has_c = (beta != 0.0f);
+  if (has_c) {
+    ok = ok && enc(&tC0, C0, m, n, 64, 32);
+    if (C1.ptr) ok = ok && enc(&tC1, C1, m, n, 64, 32);
+  }
+  ok = ok && enc(&tD0, D0, m, n, 64, 32);
+  if (D1.ptr) ok = ok && enc(&tD1, D1, m, n, 64, 32);
+  if (!ok) return CY_ERR_LAUNCH;
+  (void)bn_cta;
+
+  Params p;
+  p.M = (int)m; p.N = (int)n; p.K = (int)k; p.L = (int)L;
+  p.alpha = alpha; p.beta = beta; p.has_c = has_c ? 1 : 0;
+  p.m_blocks = (int)((m + bm - 1) / bm);
+  p.n_blocks = (int)((n + kd.bn - 1) / kd.bn);
+  p.k_blocks = (int)((k + 63) / 64);
+  p.tiles = (int)(L * p.m_blocks * p.n_blocks);
+  p.group_m = 8;
+  p.y = y;
+
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!st->attr_set[idx]) {
+      if (cudaFuncSetAttribute(kd.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kd.smem) != cudaSuccess) {
+        cudaGetLastError();
+        return CY_ERR_LAUNCH;
+      }
+      if (kd.cg == 2) cudaFuncSetAttribute(kd.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      st->attr_set[idx] = 1;
+    }
+  }
+  const int units = std::max(1, st->sms / kd.cg);
+  const int clusters = std::max(1, std::min(p.tiles, units));
+
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(clusters * kd.cg, 1, 1);
+  cfg.blockDim = dim3(kd.threads, 1, 1);
+  cfg.dynamicSmemBytes = kd.smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = kd.cg;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  void* args[] = {&tA, &tB0, &tB1, &tC0, &tC1, &tD0, &tD1, &p};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, kd.fn, args);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return CY_ERR_LAUNCH;
+  }
+  g_last.store(idx);
+  g_launches.fetch_add(1);
+  return CY_OK;
+}
+
+bool ld_ok(int64_t ld) { return ld > 0 && (ld % 8) == 0; }
+
+}  // namespace
+
+// ============================================================================================
+extern "C" {
+
+const char* cy_status_string(cy_status_t s) {
+  switch (s) {
+    case CY_OK: return "CY_OK";
+    case CY_ERR_INVALID_VALUE: return "CY_ERR_INVALID_VALUE: invalid size, leading dimension, pointer or overlap";
+    case CY_ERR_MISALIGNED: return "CY_ERR_MISALIGNED: pointer not 16-byte aligned or ld/stride not a multiple of 8";
+    case CY_ERR_UNSUPPORTED_DEVICE: return "CY_ERR_UNSUPPORTED_DEVICE: needs compute capability 10.0 (sm_100a)";
+    case CY_ERR_LAUNCH: return "CY_ERR_LAUNCH: kernel launch or TMA descriptor encode failed";
+    case CY_ERR_INTERNAL: return "CY_ERR_INTERNAL";
+  }
+  return "unknown cy_status_t";
+}
+
+int cy_num_configs(void) { return kNumGemmCfg; }
+
+cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int* stages) {
+  if (id < 0 || id >= kNumGemmCfg) return CY_ERR_INVALID_VALUE;
+  const auto& mn = menu();
+  for (const auto& k : mn)
+    if (k.var == cy::V_GEMM && k.cg == kGemmMenu[id].cg && k.bn == kGemmMenu[id].bn) {
+      if (cta_group) *cta_group = k.cg;
+      if (tile_m) *tile_m = 128 * k.cg;
+      if (tile_n) *tile_n = k.bn;
+      if (stages) *stages = k.stages;
+      return CY_OK;
+    }
+  return CY_ERR_INTERNAL;
+}
+
+cy_status_t cy_force_config(int id) {
+  if (id < -1 || id >= kNumGemmCfg) return CY_ERR_INVALID_VALUE;
+  g_forced.store(id);
+  return CY_OK;
+}
+
+int cy_last_config(void) {
+  const int idx = g_last.load();
+  if (idx < 0) return -1;
+  const auto& k = menu()[idx];
+  for (int i = 0; i < kNumGemmCfg; ++i)
+    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn) return i;
+  return -1;
+}
+
+int64_t cy_launch_count(void) { return g_launches.load(); }
+
+static cy_status_t check_common(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch) {
+  if (dt != CY_F16 && dt != CY_BF16) return CY_ERR_INVALID_VALUE;
+  if (m < 0 || n < 0 || k < 0 || batch < 0) return CY_ERR_INVALID_VALUE;
+  return CY_OK;
+}
+
+cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float alpha,
+                            const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                            int64_t strideB, float beta, const void* C, int64_t ldc, int64_t strideC, void* D,
+                            int64_t ldd, int64_t strideD, void* stream) {
+  cy_status_t s = check_common(dt, m, n, k, batch);
+  if (s != CY_OK) return s;
+  if (m == 0 || n == 0 || batch == 0) return CY_OK;
+  const bool has_c = beta != 0.0f;
+  if (!D || (k > 0 && (!A || !B)) || (has_c && !C)) return CY_ERR_INVALID_VALUE;
+  if (ldd < n || (k > 0 && (lda < k || ldb < n)) || (has_c && ldc < n)) return CY_ERR_INVALID_VALUE;
+  if (batch > 1 && (strideA < 0 || strideB < 0 || strideC < 0 || strideD < 0)) return CY_ERR_INVALID_VALUE;
+  if (batch > 1 && strideD < m * ldd) return CY_ERR_INVALID_VALUE;  // D batches must not overlap
+  if (!aligned16(D) || !ld_ok(ldd)) return CY_ERR_MISALIGNED;
+  if (k > 0 && (!aligned16(A) || !aligned16(B) || !ld_ok(lda) || !ld_ok(ldb))) return CY_ERR_MISALIGNED;
+  if (has_c && (!aligned16(C) || !ld_ok(ldc))) return CY_ERR_MISALIGNED;
+  if (batch > 1 && ((strideA % 8) || (strideB % 8) || (strideC % 8) || (strideD % 8))) return CY_ERR_MISALIGNED;
+  const Range rD = span(D, m, n, ldd, batch, strideD, 2);
+  if (k > 0 && (overlap(rD, span(A, m, k, lda, batch, strideA, 2)) || overlap(rD, span(B, k, n, ldb, batch, strideB, 2))))
+    return CY_ERR_INVALID_VALUE;
+  if (has_c && !(C == D && ldc == ldd && strideC == strideD) && overlap(rD, span(C, m, n, ldc, batch, strideC, 2)))
+    return CY_ERR_INVALID_VALUE;
+  return launch(cy::V_GEMM, dt, m, n, k, batch, alpha, {A, lda, strideA}, {B, ldb, strideB}, {nullptr, 0, 0}, beta,
+                {C, ldc, strideC}, {nullptr, 0, 0}, {D, ldd, strideD}, {nullptr, 0, 0}, nullptr, stream);
+}
+
+cy_status_t cy_gemm(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, float beta, const void* C, int64_t ldc, void* D, int64_t ldd,
+                    void* stream) {
+  return cy_gemm_batched(dt, m, n, k, 1, alpha, A, lda, 0, B, ldb, 0, beta, C, ldc, 0, D, ldd, 0, stream);
+}
+
+cy_status_t cy_dual_gemm(cy_dtype_t dt, cy_dual_mode_t mode, int64_t m, int64_t n, int64_t k, float alpha,
+                         const void* A, int64_t lda, const void* B0, int64_t ldb0, const void* B1, int64_t ldb1,
+                         float beta, const void* C0, int64_t ldc0, const void* C1, int64_t ldc1, void* D0,
+                         int64_t ldd0, void* D1, int64_t ldd1, void* stream) {
+  cy_status_t s = check_common(dt, m, n, k, 1);
+  if (s != CY_OK) return s;
+  if (mode != CY_DUAL_PAIR && mode != CY_DUAL_SUM) return CY_ERR_INVALID_VALUE;
+  const bool pair = (mode == CY_DUAL_PAIR);
+  if (!pair && (C1 || D1)) return CY_ERR_INVALID_VALUE;
+  if (m == 0 || n == 0) return CY_OK;
+  const bool has_c = beta != 0.0f;
+  if (!D0 || (pair && !D1) || (k > 0 && (!A || !B0 || !B1)) || (has_c && (!C0 || (pair && !C1))))
+    return CY_ERR_INVALID_VALUE;
+  if (ldd0 < n || (pair && ldd1 < n) || (k > 0 && (lda < k || ldb0 < n || ldb1 < n)) ||
+      (has_c && (ldc0 < n || (pair && ldc1 < n))))
+    return CY_ERR_INVALID_VALUE;
+  if (!aligned16(D0) || !ld_ok(ldd0) || (pair && (!aligned16(D1) || !ld_ok(ldd1)))) return CY_ERR_MISALIGNED;
+  if (k > 0 && (!aligned16(A) || !aligned16(B0) || !aligned16(B1) || !ld_ok(lda) || !ld_ok(ldb0) || !ld_ok(ldb1)))
+    return CY_ERR_MISALIGNED;
+  if (has_c && (!aligned16(C0) || !ld_ok(ldc0) || (pair && (!aligned16(C1) || !ld_ok(ldc1)))))
+    return CY_ERR_MISALIGNED;
+  const Range rD0 = span(D0, m, n, ldd0, 1, 0, 2);
+  const Range rD1 = pair ? span(D1, m, n, ldd1, 1, 0, 2) : Range{0, 0};
+  for (Range rd : {rD0, rD1}) {
+    if (k > 0 && (overlap(rd, span(A, m, k, lda, 1, 0, 2)) || overlap(rd, span(B0, k, n, ldb0, 1, 0, 2)) ||
+                  overlap(rd, span(B1, k, n, ldb1, 1, 0, 2))))
+      return CY_ERR_INVALID_VALUE;
+  }
+  if (overlap(rD0, rD1)) return CY_ERR_INVALID_VALUE;
+  if (has_c) {
+    if (!(C0 == D0 && ldc0 == ldd0) && overlap(rD0, span(C0, m, n, ldc0, 1, 0, 2))) return CY_ERR_INVALID_VALUE;
+    if (pair) {
+      if (!(C1 == D1 && ldc1 == ldd1) && overlap(rD1, span(C1, m, n, ldc1, 1, 0, 2))) return CY_ERR_INVALID_VALUE;
+      if (overlap(rD0, span(C1, m, n, ldc1, 1, 0, 2)) || overlap(rD1, span(C0, m, n, ldc0, 1, 0, 2)))
+        return CY_ERR_INVALID_VALUE;
+    }
+  }
+  return launch(pair ? cy::V_DUAL_PAIR : cy::V_DUAL_SUM, dt, m, n, k, 1, alpha, {A, lda, 0}, {B0, ldb0, 0},
+                {B1, ldb1, 0}, beta, {C0, ldc0, 0}, {pair ? C1 : nullptr, ldc1, 0}, {D0, ldd0, 0},
+                {pair ? D1 : nullptr, ldd1, 0}, nullptr, stream);
+}
+
+cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha, const void* A,
+                              int64_t lda, const void* B, int64_t ldb, float beta, const void* C, int64_t ldc,
+                              void* D, int64_t ldd, float* y, void* stream) {
+  cy_status_t s = check_common(dt, m, n, k, 1);
+  if (s != CY_OK) return s;
+  if (m == 0) return CY_OK;
+  if (!y) return CY_ERR_INVALID_VALUE;
+  if (n == 0) return CY_ERR_INVALID_VALUE;  // y is produced by the n-tile-0 CTAs; n == 0 has no tiles
+  const bool has_c = beta != 0.0f;
+  if (!D || (k > 0 && (!A || !B)) || (has_c && !C)) return CY_ERR_INVALID_VALUE;
+  if (ldd < n || (k > 0 && (lda < k || ldb < n)) || (has_c && ldc < n)) return CY_ERR_INVALID_VALUE;
+  if (!aligned16(D) || !ld_ok(ldd) || (reinterpret_cast<uintptr_t>(y) & 3u)) return CY_ERR_MISALIGNED;
+  if (k > 0 && (!aligned16(A) || !aligned16(B) || !ld_ok(lda) || !ld_ok(ldb))) return CY_ERR_MISALIGNED;
+  if (has_c && (!aligned16(C) || !ld_ok(ldc))) return CY_ERR_MISALIGNED;
+  const Range rD = span(D, m, n, ldd, 1, 0, 2);
+  const Range rY = span(y, 1, m, m, 1, 0, 4);
+  const Range rA = k > 0 ? span(A, m, k, lda, 1, 0, 2) : Range{0, 0};
+  const Range rB = k > 0 ? span(B, k, n, ldb, 1, 0, 2) : Range{0, 0};
+  const Range rC = has_c ? span(C, m, n, ldc, 1, 0, 2) : Range{0, 0};
+  if (overlap(rD, rA) || overlap(rD, rB) || overlap(rY, rA) || overlap(rY, rB) || overlap(rY, rC) || overlap(rY, rD))
+    return CY_ERR_INVALID_VALUE;
+  if (has_c && !(C == D && ldc == ldd) && overlap(rD, rC)) return CY_ERR_INVALID_VALUE;
+  return launch(cy::V_ROWREDUCE, dt, m, n, k, 1, alpha, {A, lda, 0}, {B, ldb, 0}, {nullptr, 0, 0}, beta,
+                {C, ldc, 0}, {nullptr, 0, 0}, {D, ldd, 0}, {nullptr, 0, 0}, y, stream);
+}
+
+}  // extern "C"

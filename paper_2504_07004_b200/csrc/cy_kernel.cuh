@@ -1,0 +1,400 @@
+// cy_kernel.cuh -- the sm_100a GEMM-family kernel: persistent, warp-specialised, TMA-fed,
+// tcgen05.mma into TMEM, optional CTA pairs (cta_group::2), fused epilogue.
+//
+// One template covers the four entry points of include/cypress_b200.h:
+//   V_GEMM       D  = alpha*A.B + beta*C                 (batched P:1520-1521)
+//   V_DUAL_PAIR  D0 = alpha*A.B0 + beta*C0, D1 = alpha*A.B1 + beta*C1   (GLU core)
+//   V_DUAL_SUM   D  = alpha*(A.B0 + A.B1) + beta*C
+//   V_ROWREDUCE  D  = alpha*A.B + beta*C and y(i) = sum_k A(i,k)
+//
+// Structure (the B200 re-derivation of the paper's warp-specialised, pipelined Hopper kernel,
+// Fig. 3b, and of the passes' end state):
+//   warp 0      producer: one lane drives TMA into an S-stage shared-memory ring (full/empty
+//               mbarriers with phase bits = the paper's modulo-indexed buffers + backwards WAR
+//               events).
+//   warp 1      MMA issuer: one lane issues tcgen05.mma (M = 128*CG, N = BN, K = 16) into a TMEM
+//               accumulator (never materialised whole elsewhere -- the paper's NONE memory,
+//               P:675-683), commits stage releases and "accumulator full" to mbarriers.
+//   warps 2-5   epilogue: TMEM -> registers (tcgen05.ld 32x32b) -> alpha/beta/cast in fp32 ->
+//               swizzled shared staging -> per-warp TMA store; double-buffered accumulators let
+//               tile i's epilogue overlap tile i+1's main loop.
+//   warps 6-9   (V_ROWREDUCE only) SIMT row-sum of the A stages while the tensor core runs
+//               (P:1580-1581); the fp32 accumulator lives in registers.
+// Tiles (prange(cdiv(M,U), cdiv(N,V))) are scheduled persistently, one CTA (pair)
+// per SM (pair), statically strided, grouped along M for L2 reuse.  CG == 2 pairs two SMs on
+// one 256-row tile: each CTA loads its half of A and half of B, the leader issues
+// tcgen05.mma.cta_group::2 (the "larger tensor core shared by pairs of SMs").
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "cy_ptx.cuh"
+
+namespace cy {
+
+enum Variant : int { V_GEMM = 0, V_DUAL_PAIR = 1, V_DUAL_SUM = 2, V_ROWREDUCE = 3 };
+
+struct Params {
+  int M, N, K, L;        // problem (L = batch count)
+  float alpha, beta;
+  int has_c;             // beta != 0: C is read
+  int m_blocks, n_blocks, k_blocks;
+  int tiles;             // L * m_blocks * n_blocks
+  int group_m;           // grouped rasterisation width (in m-blocks)
+  float* y;              // V_ROWREDUCE: y[M]
+};
+
+constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+template <int DT_, int CG_, int BN_, int STAGES_, int VAR_>
+struct Cfg {
+  static constexpr int DT = DT_;  // 0 = fp16, 1 = bf16
+  static constexpr int CG = CG_;  // CTAs per MMA (tcgen05 cta_group)
+  static constexpr int BN = BN_;  // MMA N = output tile width
+  static constexpr int STAGES = STAGES_;
+  static constexpr int VAR = VAR_;
+  static constexpr int BM_CTA = 128;          // accumulator rows per CTA = TMEM lanes
+  static constexpr int BM = BM_CTA * CG;      // MMA M = output tile height
+  static constexpr int BK = 64;               // one 128-byte swizzle atom of K per stage
+  static constexpr int UMMA_K = 16;
+  static constexpr int NUM_B = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM) ? 2 : 1;
+  static constexpr int NUM_ACC = (VAR == V_DUAL_PAIR) ? 2 : 1;
+  static constexpr int BN_CTA = BN / CG;      // B columns held per CTA
+  static constexpr int A_BYTES = BM_CTA * BK * 2;
+  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int B_ATOM_BYTES = BK * 128;  // 64 K-rows x 64 N-columns (128 B) per TMA box
+  static constexpr int STAGE_BYTES = A_BYTES + NUM_B * B_BYTES;
+  static constexpr int ACC_COLS = NUM_ACC * BN;
+  static constexpr int NUM_ACC_BUF = (2 * ACC_COLS <= 512) ? 2 : 1;
+  static constexpr int TMEM_COLS = pow2_cols(NUM_ACC_BUF * ACC_COLS);
+  static constexpr int EPI_WARPS = 4;
+  static constexpr int RED_WARPS = (VAR == V_ROWREDUCE) ? 4 : 0;
+  static constexpr int THREADS = 32 * (2 + EPI_WARPS + RED_WARPS);
+  static constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 64 columns x 2 B
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  // Row-reduce with CTA pairs: each CTA counts its own TMA bytes on its own full barrier (the
+  // reducer warps must see their local A stage land); the peer relays "full" to the leader.
+  static constexpr bool RELAY = (CG == 2 && VAR == V_ROWREDUCE);
+
+  static_assert(BN % 64 == 0 && BN_CTA % 64 == 0, "B is loaded in 64-column swizzle atoms");
+  static_assert(BN >= 64 && BN <= 256, "tcgen05 kind::f16 N range");
+  static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
+  static_assert(NUM_ACC_BUF * ACC_COLS <= 512, "TMEM has 512 columns");
+
+  // Instruction descriptor, kind::f16: c_format F32 [4,6) | a_format [7,10) | b_format [10,13) |
+  // a_major K (bit 15 = 0) | b_major MN (bit 16 = 1) | N>>3 [17,23) | M>>4 [24,29).
+  static constexpr uint32_t IDESC = (1u << 4) | (uint32_t(DT) << 7) | (uint32_t(DT) << 10) | (1u << 16) |
+                                    (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+};
+
+__device__ __forceinline__ void tile_coords(const Params& p, int t, int& b, int& mb, int& nb) {
+  const int per_b = p.m_blocks * p.n_blocks;
+  b = t / per_b;
+  const int r = t - b * per_b;
+  const int group = p.group_m * p.n_blocks;
+  const int g = r / group;
+  const int first_m = g * p.group_m;
+  const int gm = min(p.m_blocks - first_m, p.group_m);
+  const int rg = r - g * group;
+  mb = first_m + rg % gm;
+  nb = rg / gm;
+}
+
+template <int DT>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  if constexpr (DT == 0) {
+    __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+template <int DT>
+__device__ __forceinline__ float2 unpack2(uint32_t v) {
+  if constexpr (DT == 0) {
+    __half2 h = *reinterpret_cast<__half2*>(&v);
+    return __half22float2(h);
+  } else {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&v);
+    return __bfloat1622float2(h);
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    cy_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC0,
+                    const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmD0,
+                    const __grid_constant__ CUtensorMap tmD1, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-B alignment
+  const uint32_t sStage0 = base;
+  const uint32_t sEpi = base + C::STAGES * C::STAGE_BYTES;
+  const uint32_t sBar = sEpi + C::EPI_BYTES;
+  const uint32_t bFull = sBar;                               // [STAGES]
+  const uint32_t bEmpty = sBar + 8 * C::STAGES;              // [STAGES]
+  const uint32_t bPFull = sBar + 16 * C::STAGES;             // [STAGES] (RELAY only)
+  const uint32_t bTFull = sBar + 24 * C::STAGES;             // [2]
+  const uint32_t bTEmpty = bTFull + 16;                      // [2]
+  const uint32_t bCBar = bTFull + 32;                        // [4]: per-epilogue-warp C-tile loads
+  const uint32_t sTmemSlot = bTFull + 64;
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = (C::CG == 2) ? cluster_ctarank() : 0u;
+  const int cid = blockIdx.x / C::CG;
+  const int ncl = gridDim.x / C::CG;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB0);
+    if (C::NUM_B == 2) prefetch_tmap(&tmB1);
+    prefetch_tmap(&tmD0);
+    if (C::NUM_ACC == 2) prefetch_tmap(&tmD1);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(bFull + 8 * s, 1);
+      mbar_init(bEmpty + 8 * s, 1 + C::RED_WARPS);
+      if (C::RELAY) mbar_init(bPFull + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bTFull + 8 * b, 1);
+      mbar_init(bTEmpty + 8 * b, C::CG * C::EPI_WARPS);
+    }
+    for (int w = 0; w < 4; ++w) mbar_init(bCBar + 8 * w, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc<C::CG>(sTmemSlot, C::TMEM_COLS);
+    tmem_relinquish<C::CG>();
+  }
+  tc_fence_before();
+  if constexpr (C::CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer (TMA)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      constexpr bool PAIR_TMA = (C::CG == 2 && !C::RELAY);
+      for (int t = cid; t < p.tiles; t += ncl) {
+        int b, mb, nb;
+        tile_coords(p, t, b, mb, nb);
+        const int am = mb * C::BM + rank * C::BM_CTA;
+        const int bn = nb * C::BN + rank * C::BN_CTA;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(bEmpty + 8 * stage, phase ^ 1);
+          const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
+          uint32_t fb = bFull + 8 * stage;
+          if constexpr (PAIR_TMA) {
+            if (rank == 0) mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
+            fb = mapa(fb, 0);  // both CTAs count bytes on the leader's barrier
+          } else {
+            mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+          }
+          const int k0 = kb * C::BK;
+          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1) {
+            if constexpr (PAIR_TMA) tma_load_3d_pair(dst, tm, fb, c0, c1, b, pol);
+            else tma_load_3d(dst, tm, fb, c0, c1, b, pol);
+          };
+          load(sA, &tmA, k0, am);
+#pragma unroll
+          for (int j = 0; j < C::BN_CTA / 64; ++j) load(sA + C::A_BYTES + j * C::B_ATOM_BYTES, &tmB0, bn + 64 * j, k0);
+          if constexpr (C::NUM_B == 2) {
+#pragma unroll
+            for (int j = 0; j < C::BN_CTA / 64; ++j)
+              load(sA + C::A_BYTES + C::B_BYTES + j * C::B_ATOM_BYTES, &tmB1, bn + 64 * j, k0);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0 && rank == 0) {
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int t = cid; t < p.tiles; t += ncl, ++it) {
+        const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
+        const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
+        mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + buf * C::ACC_COLS;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(bFull + 8 * stage, phase);
+          if constexpr (C::RELAY) mbar_wait(bPFull + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
+          const uint32_t sB0 = sA + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
+            // A: K-major SW128, 8-row groups 1024 B apart; K advances 32 B inside the atom.
+            const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
+            // B: MN-major SW128, 64-column atoms B_ATOM_BYTES apart (LBO), 8-K-row groups 1024 B
+            // apart (SBO); K advances 16 rows = 2048 B.
+            const uint64_t bd = sdesc_sw128(sB0 + kk * 2048, C::B_ATOM_BYTES, 1024);
+            const uint32_t acc = (kb | kk) != 0;
+            mma_f16<C::CG>(d, ad, bd, C::IDESC, acc);
+            if constexpr (C::NUM_B == 2) {
+              const uint64_t bd1 = sdesc_sw128(sB0 + C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
+              if constexpr (C::VAR == V_DUAL_PAIR) mma_f16<C::CG>(d + C::BN, ad, bd1, C::IDESC, acc);
+              else mma_f16<C::CG>(d, ad, bd1, C::IDESC, 1u);
+            }
+          }
+          mma_commit<C::CG>(bEmpty + 8 * stage, 0x3);  // frees the stage in both CTAs
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit<C::CG>(bTFull + 8 * buf, 0x3);      // accumulator ready, both CTAs
+      }
+    } else if (C::RELAY && lane == 0 && rank == 1) {
+      // peer CTA: relay "my stage landed" to the leader's second full barrier
+      uint32_t stage = 0, phase = 0;
+      const uint32_t pf0 = mapa(bPFull, 0);
+      for (int t = cid; t < p.tiles; t += ncl)
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(bFull + 8 * stage, phase);
+          mbar_arrive_cluster(pf0 + 8 * stage);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+    }
+  } else if (warp < 2 + C::EPI_WARPS) {
+    // ------------------------------------------------------------------ epilogue
+    const int ew = warp - 2;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t sE = sEpi + ew * 2 * C::EPI_BUF_BYTES;
+    const uint32_t cbar = bCBar + 8 * ew;
+    const uint64_t pol = policy_evict_normal();
+    uint32_t slot = 0, cphase = 0;
+    int it = 0;
+    for (int t = cid; t < p.tiles; t += ncl, ++it) {
+      int b, mb, nb;
+      tile_coords(p, t, b, mb, nb);
+      const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
+      const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
+      mbar_wait(bTFull + 8 * buf, bph);
+      tc_fence_after();
+      const int row0 = mb * C::BM + rank * C::BM_CTA + 32 * q;
+#pragma unroll 1
+      for (int a = 0; a < C::NUM_ACC; ++a) {
+        const CUtensorMap* tmD = (a == 0) ? &tmD0 : &tmD1;
+        const CUtensorMap* tmC = (a == 0) ? &tmC0 : &tmC1;
+#pragma unroll 1
+        for (int c = 0; c < C::BN / 64; ++c) {
+          const int n0 = nb * C::BN + 64 * c;
+          const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last used this slot has read it
+          __syncwarp();
+          if (p.has_c) {
+            if (lane == 0) {
+              mbar_arrive_expect_tx(cbar, C::EPI_BUF_BYTES);
+              tma_load_3d(sb, tmC, cbar, n0, row0, b, pol);
+            }
+            mbar_wait(cbar, cphase);
+            cphase ^= 1;
+          }
+          uint32_t r0[32], r1[32];
+          if (p.k_blocks > 0) {
+            const uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + buf * C::ACC_COLS + a * C::BN + 64 * c;
+            tmem_ld_32x32b_x32(ta, r0);
+            tmem_ld_32x32b_x32(ta + 32, r1);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r0[i] = r1[i] = 0u;
+          }
+          const uint32_t row_addr = sb + lane * 128;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const uint32_t addr = row_addr + ((v ^ (lane & 7)) << 4);  // SWIZZLE_128B chunk
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = 8 * v + e;
+              f[e] = __uint_as_float(col < 32 ? r0[col] : r1[col - 32]) * p.alpha;
+            }
+            if (p.has_c) {
+              uint32_t cv[4];
+              ld_shared_v4(addr, cv[0], cv[1], cv[2], cv[3]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 cf = unpack2<C::DT>(cv[e]);
+                f[2 * e] = fmaf(p.beta, cf.x, f[2 * e]);
+                f[2 * e + 1] = fmaf(p.beta, cf.y, f[2 * e + 1]);
+              }
+            }
+            st_shared_v4(addr, pack2<C::DT>(f[0], f[1]), pack2<C::DT>(f[2], f[3]), pack2<C::DT>(f[4], f[5]),
+                         pack2<C::DT>(f[6], f[7]));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(tmD, sb, n0, row0, b);
+            bulk_commit();
+          }
+          slot ^= 1;
+        }
+      }
+      // every tcgen05.ld of this accumulator buffer has completed (wait::ld above)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * buf, 0));
+        else mbar_arrive(bTEmpty + 8 * buf);
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  } else {
+    // ------------------------------------------------------------------ row reduction (SIMT)
+    const int q = warp & 3;
+    const int r = 32 * q + lane;  // row of this CTA's 128-row A stage
+    uint32_t stage = 0, phase = 0;
+    for (int t = cid; t < p.tiles; t += ncl) {
+      int b, mb, nb;
+      tile_coords(p, t, b, mb, nb);
+      const bool do_red = (nb == 0);  // one n-tile per row block reduces: no atomics, deterministic
+      float acc = 0.f;
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(bFull + 8 * stage, phase);
+        if (do_red) {
+          const uint32_t row_addr = sStage0 + stage * C::STAGE_BYTES + r * 128;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {  // logical 16-B chunk v = K elements 8v..8v+7, in k order
+            uint32_t x[4];
+            ld_shared_v4(row_addr + ((v ^ (r & 7)) << 4), x[0], x[1], x[2], x[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = unpack2<C::DT>(x[e]);
+              acc += f.x;
+              acc += f.y;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bEmpty + 8 * stage);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (do_red) {
+        const int row = mb * C::BM + rank * C::BM_CTA + r;
+        if (row < p.M) p.y[(size_t)b * p.M + row] = acc;
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  if constexpr (C::CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::CG>(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace cy

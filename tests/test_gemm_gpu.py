@@ -1,0 +1,301 @@
+"""GPU parity tests: the sm_100a kernels (through the C ABI) vs the fp64 oracle.
+
+Bars (BASELINE.json north_star): integer-valued inputs bit-exact against RN(oracle);
+seeded uniform[-1,1] inputs within |D - D_ref| <= 2^-8|D_ref| + 1e-3 sqrt(K) per element.
+Sizes span several tiles plus ragged tails; full-size configurations are checked on
+oracle-sampled rows in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import assert_bits_equal, assert_within_tol, decode, to_bits, to_dev
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2504_07004_b200 as cy  # noqa: E402
+
+NCFG = cy.num_configs()
+ALL_CFGS = list(range(NCFG))
+
+
+@pytest.fixture(autouse=True)
+def _reset_config():
+    cy.force_config(-1)
+    yield
+    cy.force_config(-1)
+
+
+def run_gemm(A, B, C, alpha, beta, dtype, cfg=-1):
+    cy.force_config(cfg)
+    dA, dB = to_dev(A, dtype), to_dev(B, dtype)
+    dC = to_dev(C, dtype) if C is not None else None
+    D = cy.gemm(dA, dB, dC, alpha, beta)
+    torch.cuda.synchronize()
+    return to_bits(D)
+
+
+# ---------------------------------------------------------------- integer: bit-exact, every config
+INT_SHAPES = [(256, 256, 256), (1, 1, 1), (7, 9, 13), (64, 65, 127), (129, 257, 255), (300, 520, 200),
+              (1000, 1023, 129), (513, 384, 1000)]
+
+
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+@pytest.mark.parametrize("shape", INT_SHAPES)
+def test_gemm_integer_bit_exact(cfg, shape):
+    m, n, k = shape
+    A, B, C = synth.gemm_inputs(m, n, k, seed=synth.seed_for(0, 10) + m, kind="int", with_c=True)
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16", cfg)
+    assert_bits_equal(D, oracle.encode("f16", oracle.gemm("f16", A, B)), f"cfg{cfg} {shape}")
+    assert cy.last_config() == cfg
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+def test_gemm_integer_alpha_beta_bit_exact(dtype, cfg):
+    m, n, k = 200, 300, 136
+    A, B, C = synth.gemm_inputs(m, n, k, seed=77, dtype=dtype, kind="int", with_c=True)
+    D = run_gemm(A, B, C, 2.0, -3.0, dtype, cfg)
+    assert_bits_equal(D, oracle.encode(dtype, oracle.gemm(dtype, A, B, C, 2.0, -3.0)), f"{dtype} cfg{cfg}")
+
+
+def test_gemm_config_invariance_integer():
+    """P:278 'mapping decisions can only affect performance': every config, same bits."""
+    A, B, _ = synth.gemm_inputs(777, 600, 520, seed=5, kind="int")
+    outs = [run_gemm(A, B, None, 1.0, 0.0, "f16", c) for c in ALL_CFGS]
+    for c in range(1, len(outs)):
+        assert_bits_equal(outs[c], outs[0], f"cfg{c} vs cfg0")
+
+
+# ---------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+def test_identity_and_permutation(cfg):
+    k = 384
+    _, B, _ = synth.gemm_inputs(k, 320, k, seed=21)
+    I = synth.f64_to_bits(np.eye(k), "f16")
+    assert_bits_equal(run_gemm(I, B, None, 1.0, 0.0, "f16", cfg), B, "A = I")
+    perm = np.random.default_rng(cfg).permutation(k)
+    P = synth.f64_to_bits(np.eye(k)[perm], "f16")
+    assert_bits_equal(run_gemm(P, B, None, 1.0, 0.0, "f16", cfg), B[perm], "A = P")
+    A, _, _ = synth.gemm_inputs(260, k, k, seed=22)
+    Q = synth.f64_to_bits(np.eye(k)[:, perm], "f16")
+    assert_bits_equal(run_gemm(A, Q, None, 1.0, 0.0, "f16", cfg), A[:, perm], "B = Q")
+
+
+def test_k1_outer_product_single_rounding():
+    A, B, _ = synth.gemm_inputs(300, 200, 1, seed=41)
+    # K=1 needs lda >= 8 for TMA: pad A's rows
+    Ap = np.zeros((300, 8), np.uint16)
+    Ap[:, :1] = A
+    dA = to_dev(Ap, "f16")[:, :1]
+    D = to_bits(cy.gemm(dA, to_dev(B, "f16")))
+    assert_bits_equal(D, oracle.encode("f16", oracle.gemm("f16", A, B)), "K=1")
+
+
+# ---------------------------------------------------------------- random: tolerance
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("seed", range(3))
+def test_gemm_256_random(dtype, seed):
+    """BASELINE configs[0]: 256^3 vs the fp64 oracle, seeded uniform[-1,1]."""
+    A, B, C = synth.gemm_inputs(256, 256, 256, seed=synth.seed_for(0, seed), dtype=dtype, with_c=True)
+    D = run_gemm(A, B, None, 1.0, 0.0, dtype)
+    assert_within_tol(D, oracle.gemm(dtype, A, B), 256, dtype, what="256^3")
+
+
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+@pytest.mark.parametrize("shape", [(1000, 1023, 129), (520, 392, 1111), (4096, 4096, 4096)])
+def test_gemm_random_tolerance(cfg, shape):
+    m, n, k = shape
+    A, B, C = synth.gemm_inputs(m, n, k, seed=synth.seed_for(1, cfg), with_c=True)
+    rows = None if m * n * k <= 2 ** 31 else synth.sample_rows(m)
+    D = run_gemm(A, B, C, 1.0, 1.0, "f16", cfg)
+    ref = oracle.gemm("f16", A, B, C, 1.0, 1.0, rows=rows)
+    assert_within_tol(D if rows is None else D[rows], ref, k, "f16", what=f"cfg{cfg} {shape}")
+
+
+def test_gemm_deterministic():
+    A, B, _ = synth.gemm_inputs(1024, 1024, 2048, seed=3)
+    d1 = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    d2 = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    assert_bits_equal(d1, d2, "repeat")
+
+
+# ---------------------------------------------------------------- contract / edge cases
+def test_alpha0_beta1_is_c_and_c_alias_d():
+    A, B, C = synth.gemm_inputs(300, 260, 70, seed=91, with_c=True)
+    dC = to_dev(C, "f16")
+    D = cy.gemm(to_dev(A, "f16"), to_dev(B, "f16"), dC, 0.0, 1.0)
+    assert_bits_equal(to_bits(D), C, "alpha=0, beta=1")
+    # C == D alias: D = A.B + D
+    ref = oracle.encode("f16", oracle.gemm("f16", A, B, C, 1.0, 1.0))
+    cy.gemm(to_dev(A, "f16"), to_dev(B, "f16"), dC, 1.0, 1.0, out=dC)
+    torch.cuda.synchronize()
+    want = oracle.gemm("f16", A, B, C, 1.0, 1.0)
+    assert_within_tol(to_bits(dC), want, 70, "f16", what="C aliases D")
+    del ref
+
+
+def test_beta0_does_not_read_c():
+    A, B, _ = synth.gemm_inputs(256, 256, 64, seed=92, kind="int")
+    nanC = torch.full((256, 256), float("nan"), dtype=torch.float16, device="cuda")
+    D = cy.gemm(to_dev(A, "f16"), to_dev(B, "f16"), nanC, 1.0, 0.0)
+    assert_bits_equal(to_bits(D), oracle.encode("f16", oracle.gemm("f16", A, B)), "beta=0 NaN C")
+
+
+def test_k0_gives_beta_c():
+    _, _, C = synth.gemm_inputs(130, 270, 1, seed=93, with_c=True)
+    A = torch.empty((130, 0), dtype=torch.float16, device="cuda")
+    B = torch.empty((0, 270), dtype=torch.float16, device="cuda")
+    D = cy.gemm(A, B, to_dev(C, "f16"), 1.0, 0.5)
+    assert_bits_equal(to_bits(D), oracle.encode("f16", 0.5 * decode(C, "f16")), "k=0")
+    D0 = cy.gemm(A, B)  # beta = 0, k = 0 -> zeros
+    assert not to_bits(D0).any()
+
+
+def test_canary_padding_untouched():
+    m, n, k = 200, 136, 96
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=94)
+    big = torch.full((m + 9, n + 24), 1234.0, dtype=torch.float16, device="cuda")
+    out = big[:m, :n]
+    cy.gemm(to_dev(A, "f16"), to_dev(B, "f16"), out=out)
+    torch.cuda.synchronize()
+    full = to_bits(big)
+    assert_within_tol(full[:m, :n], oracle.gemm("f16", A, B), k, "f16", what="strided D")
+    canary = np.float16(1234.0).view(np.uint16)
+    assert (full[:m, n:] == canary).all() and (full[m:, :] == canary).all()
+
+
+def test_misaligned_ld_rejected():
+    A = torch.zeros((16, 12), dtype=torch.float16, device="cuda")
+    B = torch.zeros((12, 16), dtype=torch.float16, device="cuda")
+    with pytest.raises(cy.CyError) as e:
+        cy.gemm(A, B)
+    assert e.value.name == "CY_ERR_MISALIGNED"
+
+
+# ---------------------------------------------------------------- batched
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+def test_batched_matches_oracle_and_slices(cfg):
+    L, m, n, k = 5, 300, 260, 200
+    A, B, C = synth.gemm_inputs(m, n, k, seed=101, batch=L, with_c=True)
+    cy.force_config(cfg)
+    D = to_bits(cy.gemm_batched(to_dev(A, "f16"), to_dev(B, "f16"), to_dev(C, "f16"), 1.0, 1.0))
+    assert_within_tol(D, oracle.gemm_batched("f16", A, B, C, 1.0, 1.0), k, "f16", what=f"batched cfg{cfg}")
+    for b in (0, L - 1):
+        assert_bits_equal(D[b], run_gemm(A[b], B[b], C[b], 1.0, 1.0, "f16", cfg), f"slice {b}")
+
+
+def test_batched_64x1024_integer():
+    """BASELINE configs[2] shape (64 x 1024^3), integer inputs: bit-exact."""
+    L = 64
+    A, B, _ = synth.gemm_inputs(1024, 1024, 1024, seed=102, batch=L, kind="int")
+    D = to_bits(cy.gemm_batched(to_dev(A, "f16"), to_dev(B, "f16")))
+    want = oracle.encode("f16", oracle.gemm_batched("f16", A[:4], B[:4]))
+    assert_bits_equal(D[:4], want, "batched 64x1024^3 first 4")
+    want_last = oracle.encode("f16", oracle.gemm("f16", A[-1], B[-1]))
+    assert_bits_equal(D[-1], want_last, "last batch")
+
+
+# ---------------------------------------------------------------- dual GEMM
+@pytest.mark.parametrize("cfg", [-1, 0, 1, 3])
+@pytest.mark.parametrize("shape", [(256, 256, 256), (333, 300, 190)])
+def test_dual_pair(cfg, shape):
+    m, n, k = shape
+    A, B0, B1, C0, C1 = synth.dual_inputs(m, n, k, seed=111, with_c=True)
+    cy.force_config(cfg)
+    d0, d1 = cy.dual_gemm(*(to_dev(x, "f16") for x in (A, B0, B1, C0, C1)), alpha=1.0, beta=0.5, mode="pair")
+    r0, r1 = oracle.dual_gemm("f16", "pair", A, B0, B1, C0, C1, 1.0, 0.5)
+    assert_within_tol(to_bits(d0), r0, k, "f16", what="D0")
+    assert_within_tol(to_bits(d1), r1, k, "f16", what="D1")
+
+
+@pytest.mark.parametrize("cfg", [-1, 0, 1, 3])
+def test_dual_sum_and_invariants(cfg):
+    m, n, k = 300, 264, 200
+    A, B0, B1, C0, _ = synth.dual_inputs(m, n, k, seed=112, with_c=True)
+    cy.force_config(cfg)
+    dA, dB0, dB1, dC = (to_dev(x, "f16") for x in (A, B0, B1, C0))
+    D = cy.dual_gemm(dA, dB0, dB1, dC, alpha=1.0, beta=1.0, mode="sum")
+    assert_within_tol(to_bits(D), oracle.dual_gemm("f16", "sum", A, B0, B1, C0, None, 1.0, 1.0), k, "f16",
+                      sum_terms=2, what="sum")
+    # SUM with B1 = 0 equals GEMM bit-exactly (adding exact zeros in fp32)
+    Z = torch.zeros_like(dB1)
+    Ds = to_bits(cy.dual_gemm(dA, dB0, Z, mode="sum"))
+    cy.force_config(cfg)
+    assert_bits_equal(Ds, to_bits(cy.gemm(dA, dB0)), "sum with B1=0 vs gemm")
+    # PAIR with B0 == B1 gives D0 == D1
+    d0, d1 = cy.dual_gemm(dA, dB0, dB0.clone(), mode="pair")
+    assert_bits_equal(to_bits(d0), to_bits(d1), "pair B0 == B1")
+
+
+def test_dual_integer_bit_exact():
+    A, B0, B1, _, _ = synth.dual_inputs(520, 384, 300, seed=113, kind="int")
+    dA, dB0, dB1 = (to_dev(x, "f16") for x in (A, B0, B1))
+    d0, d1 = cy.dual_gemm(dA, dB0, dB1, mode="pair")
+    r0, r1 = oracle.dual_gemm("f16", "pair", A, B0, B1)
+    assert_bits_equal(to_bits(d0), oracle.encode("f16", r0), "pair D0")
+    assert_bits_equal(to_bits(d1), oracle.encode("f16", r1), "pair D1")
+    Ds = cy.dual_gemm(dA, dB0, dB1, mode="sum")
+    assert_bits_equal(to_bits(Ds), oracle.encode("f16", oracle.dual_gemm("f16", "sum", A, B0, B1)), "sum")
+
+
+# ---------------------------------------------------------------- GEMM + row reduction
+@pytest.mark.parametrize("cfg", [-1, 0, 1, 3])
+@pytest.mark.parametrize("shape", [(256, 256, 256), (1000, 520, 333)])
+def test_rowreduce(cfg, shape):
+    m, n, k = shape
+    A, B, C = synth.gemm_inputs(m, n, k, seed=121, with_c=True)
+    cy.force_config(cfg)
+    D, y = cy.gemm_rowreduce(to_dev(A, "f16"), to_dev(B, "f16"), to_dev(C, "f16"), 1.5, -0.5)
+    torch.cuda.synchronize()
+    assert_within_tol(to_bits(D), oracle.gemm("f16", A, B, C, 1.5, -0.5), k, "f16", what="D")
+    yref = oracle.rowsum("f16", A)
+    assert (np.abs(y.cpu().numpy() - yref) <= oracle.tolerance(yref, k)).all()
+
+
+def test_rowreduce_integer_and_invariants():
+    m, n, k = 700, 300, 513
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=122, kind="int")
+    dA = to_dev(A, "f16")
+    D, y = cy.gemm_rowreduce(dA, to_dev(B, "f16"))
+    assert_bits_equal(to_bits(D), oracle.encode("f16", oracle.gemm("f16", A, B)), "D int")
+    assert np.array_equal(y.cpu().numpy().astype(np.float64), oracle.rowsum("f16", A))
+    # y independent of B / alpha / beta
+    _, B2, C2 = synth.gemm_inputs(m, n, k, seed=123, with_c=True)
+    _, y2 = cy.gemm_rowreduce(dA, to_dev(B2, "f16"), to_dev(C2, "f16"), 0.25, 2.0)
+    assert torch.equal(y, y2)
+    # all-ones A: y = K exactly
+    ones = torch.ones((256, 640), dtype=torch.float16, device="cuda")
+    _, y3 = cy.gemm_rowreduce(ones, torch.zeros((640, n), dtype=torch.float16, device="cuda"))
+    assert (y3 == 640.0).all()
+
+
+# ---------------------------------------------------------------- full-size (bench launch configs), sampled
+def test_full_8192_sampled():
+    """BASELINE configs[1] 8192^3 (the bench workload), oracle on sampled rows."""
+    n = 8192
+    A, B, _ = synth.gemm_inputs(n, n, n, seed=synth.seed_for(1, 0))
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    rows = synth.sample_rows(n, n_random=16)
+    ref = oracle.gemm("f16", A, B, rows=rows)
+    assert_within_tol(D[rows], ref, n, "f16", what="8192^3 sampled")
+
+
+def test_full_rowreduce_65536_sampled():
+    """BASELINE configs[4] (65536 x 8192 x 8192, fused row reduction) as one single-GPU launch,
+    oracle on sampled rows."""
+    m, n, k = 65536, 8192, 8192
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=synth.seed_for(4, 0))
+    D, y = cy.gemm_rowreduce(to_dev(A, "f16"), to_dev(B, "f16"))
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(m, tile=256, n_random=8)[::4]
+    D_s = to_bits(D)[rows]
+    ref = oracle.gemm("f16", A, B, rows=rows)
+    assert_within_tol(D_s, ref, k, "f16", what="65536 rowreduce D")
+    yref = oracle.rowsum("f16", A, rows=rows)
+    assert (np.abs(y.cpu().numpy()[rows] - yref) <= oracle.tolerance(yref, k)).all()
