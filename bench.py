@@ -1,0 +1,516 @@
+"""bench.py -- headline benchmark of the B200 Cypress GEMM family.
+
+Default workload (BASELINE.json metric, configs[1] at its 8192^3 point, M-sharded to P GPUs
+as in configs[4]): every rank computes an 8192 x 8192 x 8192 fp16 GEMM (its M-row shard of a
+(8192*P) x 8192 x 8192 problem, B replicated) through the C ABI.  A step = one cy_gemm call
+(host entry -> TMA descriptors -> one persistent tcgen05 kernel), i.e. every row a1-a6 of
+SURVEY.md section 8(a).  No collective is on the data path (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
+
+Other workloads (--workload): sweep-<n> (n^3), batched (64 x 1024^3, batch-sharded),
+dual (dual-GEMM pair 8192^3), rowreduce (65536/P x 8192 x 8192 + y), allgather
+(rowreduce + NCCL all-gather of D and y, replicated result).
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream, W warm-up
+steps, barrier + synchronize on both sides of exactly K timed steps, max over ranks.
+L2: inputs rotate over two input sets whose total exceeds the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp16 GEMM TFLOP/s per B200 and % of dense tensor peak; 8-GPU aggregate"
+
+
+# ----------------------------------------------------------------------------- helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"burst": d.get("bf16_tflops", 1590.0), "sustained": d.get("bf16_tflops_sustained", 1400.0),
+                "source": "measured (MEASURED_PEAKS.json, cuBLAS bf16; fp16 dense peak = bf16 dense peak)"}
+    return {"burst": 1590.0, "sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md: 1.59 PF burst / ~1.4 PF sustained)"}
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(workload)
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock / power / clock-event reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, dev_index, period=0.005):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self.period = period
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                self.samples.append((mhz, r, pw))
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        mhz = [s[0] for s in self.samples]
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(mhz), "power_w_max": round(max(s[2] for s in self.samples), 1),
+                "sm_mhz_min": min(mhz)}
+
+    def rejected(self):
+        bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+        s = self.summary()
+        if self.reasons & bad:
+            return True
+        if s["sm_mhz"] and self.max_mhz and s["sm_mhz"] < 0.5 * self.max_mhz and not self.reasons:
+            return True
+        return False
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------- workloads
+def make_workload(name, rank, world, device):
+    """Returns dict with: flops_per_step (this rank), step(i) callable, e2e_step(i) callable,
+    h2d/d2h bytes, oracle sampler, description."""
+    import numpy as np
+    import torch
+
+    import paper_2504_07004_b200 as cy
+    import synth
+
+    def up(bits):
+        return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.float16).to(device)
+
+    def pinned(bits):
+        t = torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.float16)
+        return t.pin_memory()
+
+    W = {}
+    if name in ("gemm", "rowreduce", "allgather") or name.startswith("sweep-"):
+        if name.startswith("sweep-"):
+            n = int(name.split("-")[1])
+            m_rank, k = n, n
+            desc = f"fp16 GEMM {n}^3 (configs[1] sweep point), 1 GPU" if world == 1 else \
+                f"fp16 GEMM ({n}*P) x {n} x {n}, M-sharded over P={world}"
+        elif name == "gemm":
+            n = k = 8192
+            m_rank = 8192
+            desc = ("fp16 GEMM 8192^3 (configs[1] 8192 point)" if world == 1 else
+                    f"fp16 GEMM {8192 * world} x 8192 x 8192 M-sharded over {world} GPUs (configs[4] shape, no reduction)")
+        else:
+            n = k = 8192
+            m_rank = 65536 // world
+            desc = (f"fp16 GEMM 65536 x 8192 x 8192 + fused row reduction y(i)=sum_k A(i,k) (configs[4]), "
+                    f"M-sharded over {world} GPU(s)" + (", NCCL all-gather of D and y (replicated)" if name == "allgather" else ""))
+        sets = []
+        host_sets = []
+        nsets = 2 if m_rank * k * 2 + k * n * 2 < 400e6 else 1
+        for s in range(nsets):
+            A = synth.uniform((m_rank, k), synth.seed_for(4 if name in ("rowreduce", "allgather") else 1, 10 * rank + s))
+            B = synth.uniform((k, n), synth.seed_for(1, 1000 + s))  # replicated across ranks
+            host_sets.append((A, B))
+            sets.append((up(A), up(B)))
+        D = torch.empty((m_rank, n), dtype=torch.float16, device=device)
+        y = torch.empty((m_rank,), dtype=torch.float32, device=device)
+        flops = 2.0 * m_rank * n * k
+        if name == "gemm" or name.startswith("sweep-"):
+            def step(i):
+                a, b = sets[i % nsets]
+                cy.gemm(a, b, out=D)
+        elif name == "rowreduce":
+            def step(i):
+                a, b = sets[i % nsets]
+                cy.gemm_rowreduce(a, b, out=D, y=y)
+        else:
+            import torch.distributed as dist
+
+            Dfull = torch.empty((m_rank * world, n), dtype=torch.float16, device=device)
+            yfull = torch.empty((m_rank * world,), dtype=torch.float32, device=device)
+
+            def step(i):
+                a, b = sets[i % nsets]
+                cy.gemm_rowreduce(a, b, out=D, y=y)
+                if world > 1:
+                    dist.all_gather_into_tensor(Dfull, D)
+                    dist.all_gather_into_tensor(yfull, y)
+        hA = [pinned(h[0]) for h in host_sets]
+        hB = [pinned(h[1]) for h in host_sets]
+        hD = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
+
+        def e2e_step(i):
+            j = i % nsets
+            a = hA[j].to(device, non_blocking=True)
+            b = hB[j].to(device, non_blocking=True)
+            if name in ("rowreduce", "allgather"):
+                cy.gemm_rowreduce(a, b, out=D, y=y)
+            else:
+                cy.gemm(a, b, out=D)
+            hD.copy_(D, non_blocking=True)
+
+        W.update(flops=flops, step=step, e2e_step=e2e_step, desc=desc,
+                 h2d=hA[0].numel() * 2 + hB[0].numel() * 2, d2h=hD.numel() * 2,
+                 shape={"m": m_rank * world, "n": n, "k": k, "m_per_gpu": m_rank},
+                 oracle_case=("gemm", host_sets[0]), kernel_flops=flops)
+    elif name == "batched":
+        L_total, m = 64, 1024
+        L = L_total // world
+        A = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank))
+        B = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 1))
+        A2 = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 2))
+        B2 = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 3))
+        sets = [(up(A), up(B)), (up(A2), up(B2))]
+        D = torch.empty((L, m, m), dtype=torch.float16, device=device)
+
+        def step(i):
+            a, b = sets[i % 2]
+            cy.gemm_batched(a, b, out=D)
+        hA, hB = pinned(A), pinned(B)
+        hD = torch.empty((L, m, m), dtype=torch.float16).pin_memory()
+
+        def e2e_step(i):
+            cy.gemm_batched(hA.to(device, non_blocking=True), hB.to(device, non_blocking=True), out=D)
+            hD.copy_(D, non_blocking=True)
+        W.update(flops=2.0 * L * m ** 3, step=step, e2e_step=e2e_step,
+                 desc=f"batched fp16 GEMM 64 x 1024^3 (configs[2]), batch-sharded over {world} GPU(s)",
+                 h2d=2 * hA.numel() * 2, d2h=hD.numel() * 2, shape={"batch": L_total, "m": m, "n": m, "k": m},
+                 oracle_case=("batched", (A, B)), kernel_flops=2.0 * L * m ** 3)
+    elif name == "dual":
+        n = 8192
+        m_rank = n // world if world > 1 else n
+        A = synth.uniform((m_rank, n), synth.seed_for(3, 10 * rank))
+        B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
+        B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
+        dA, dB0, dB1 = up(A), up(B0), up(B1)
+        D0 = torch.empty((m_rank, n), dtype=torch.float16, device=device)
+        D1 = torch.empty_like(D0)
+
+        def step(i):
+            cy.dual_gemm(dA, dB0, dB1, mode="pair", out0=D0, out1=D1)
+        hA, hB0, hB1 = pinned(A), pinned(B0), pinned(B1)
+        hD0 = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
+        hD1 = torch.empty_like(hD0).pin_memory()
+
+        def e2e_step(i):
+            cy.dual_gemm(hA.to(device, non_blocking=True), hB0.to(device, non_blocking=True),
+                         hB1.to(device, non_blocking=True), mode="pair", out0=D0, out1=D1)
+            hD0.copy_(D0, non_blocking=True)
+            hD1.copy_(D1, non_blocking=True)
+        W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
+                 desc=f"dual-GEMM D=(A*B0, A*B1), 8192^3 (configs[3])" + (f", M-sharded over {world}" if world > 1 else ""),
+                 h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=2 * hD0.numel() * 2,
+                 shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("dual", (A, B0, B1)),
+                 kernel_flops=4.0 * m_rank * n * n)
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return W
+
+
+def oracle_baseline(case, budget_s=12.0):
+    """Time the fp64 C oracle, as it stands, on a bounded row sample of the same workload."""
+    import numpy as np
+
+    import oracle
+
+    kind, arrs = case
+    nth = oracle.num_threads()
+    if kind == "batched":
+        A, B = arrs
+        L = A.shape[0]
+        t0 = time.perf_counter()
+        used = 0
+        for b in range(L):
+            oracle.gemm("f16", A[b], B[b])
+            used += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        m = A.shape[1]
+        flops = 2.0 * used * m ** 3
+        return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
+                "sample": f"{used} of {L} batches of 1024^3 (full GEMMs), fp64 C oracle, {dt:.1f} s"}
+    if kind == "dual":
+        A, B0, B1 = arrs
+        fn = lambda rows: oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows)  # noqa: E731
+        per_row = 4.0 * B0.shape[1] * A.shape[1]
+    else:
+        A, B = arrs
+        fn = lambda rows: oracle.gemm("f16", A, B, rows=rows)  # noqa: E731
+        per_row = 2.0 * B.shape[1] * A.shape[1]
+    m = A.shape[0]
+    # calibrate on a few rows, then size the sample to ~budget_s
+    probe = np.arange(min(m, max(2 * nth, 8)))
+    t0 = time.perf_counter()
+    fn(probe)
+    dt0 = time.perf_counter() - t0
+    nrows = int(min(m, max(len(probe), len(probe) * budget_s / max(dt0, 1e-3))))
+    rows = np.linspace(0, m - 1, nrows).astype(np.int64)
+    t0 = time.perf_counter()
+    fn(rows)
+    dt = time.perf_counter() - t0
+    return {"value": per_row * nrows / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
+            "sample": f"{nrows} of {m} rows (all columns, full K) of the same inputs, fp64 C oracle, {dt:.1f} s"}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="gemm")
+    ap.add_argument("--impl", default="cypress_b200", choices=["cypress_b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+    import paper_2504_07004_b200 as cy
+
+    W = make_workload(args.workload, rank, world, device)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def maxred(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps, warmup, sample_clocks=True):
+        for i in range(warmup):
+            fn(i)
+        barrier()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        n0 = cy.launch_count()
+        sampler = ClockSampler(local)
+        with sampler:
+            barrier()
+            for i in range(steps):
+                starts[i].record(stream)
+                fn(warmup + i)
+                ends[i].record(stream)
+            barrier()
+        launches = cy.launch_count() - n0
+        total_ms = starts[0].elapsed_time(ends[-1])
+        per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        return total_ms, per, launches, sampler
+
+    attempts = 0
+    while True:
+        attempts += 1
+        total_ms, per, launches, sampler = timed(W["step"], args.steps, args.warmup)
+        if not sampler.rejected() or attempts >= 2:
+            break
+    total_ms = maxred(total_ms)
+    kern_ms = maxred(statistics.mean(per))
+    ms_per_step = total_ms / args.steps
+    value = W["flops"] * world / (ms_per_step * 1e-3) / 1e12
+    peaks = load_peaks()
+    achieved = W["kernel_flops"] / (kern_ms * 1e-3) / 1e12
+    peak = peaks["burst"]
+
+    e2e = None
+    if not args.no_e2e:
+        e_steps = max(3, min(args.steps, 20))
+        e_total, _, _, _ = timed(W["e2e_step"], e_steps, 3)
+        e_total = maxred(e_total)
+        e2e = {"value": W["flops"] * world / (e_total / e_steps * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(W["h2d"]), "d2h_bytes_per_step": int(W["d2h"]),
+               "ms_per_step": e_total / e_steps, "path": "pinned host -> device copies + C-ABI call + D -> pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(W["oracle_case"])
+
+    if rank == 0:
+        kcfg = cy.last_config()
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
+            "config": {"workload": W["desc"], **W["shape"],
+                       "parallelism": f"M-row shards x{world}, B replicated, no collective" if args.workload != "allgather" else f"M-row shards x{world} + NCCL all-gather",
+                       "l2": "inputs rotate over 2 sets (> 126 MB L2 total)" if W["flops"] > 1e12 or args.workload == "batched" else "inputs rotate over 2 sets",
+                       "kernel_config": cy.config_info(kcfg) if kcfg >= 0 else None},
+            "pct_of_dense_peak": round(100.0 * value / world / peak, 2),
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(achieved / peak, 4), "traffic": load_traffic(args.workload),
+                         "peak_source": peaks["source"] + "; burst figure (kernel timed alone, back to back)",
+                         "frac_of_sustained": round(achieved / peaks["sustained"], 4),
+                         "kernel_ms": round(kern_ms, 5)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": sampler.summary(),
+            "timing": "CUDA events on the launching stream; barrier+sync both sides; max over ranks",
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the fp64 CPU oracle (the only reference this tier has), timed as it
+    stands on the host cores, on a bounded sample of the same workload per step."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    import synth
+
+    oracle.build()
+    name = args.workload
+    if name == "gemm" or name.startswith("sweep-"):
+        n = 8192 if name == "gemm" else int(name.split("-")[1])
+        A = synth.uniform((n, n), synth.seed_for(1, 0))
+        B = synth.uniform((n, n), synth.seed_for(1, 1000))
+        per_row = 2.0 * n * n
+        fn = lambda rows: oracle.gemm("f16", A, B, rows=rows)  # noqa: E731
+        m = n
+        desc = f"fp16 GEMM {n}^3" + (f" x{world} M-shards" if world > 1 else "")
+    elif name in ("rowreduce", "allgather"):
+        m, n = 65536, 8192
+        A = synth.uniform((2048, n), synth.seed_for(4, 0))  # the sampled rows come from this block
+        B = synth.uniform((n, n), synth.seed_for(1, 1000))
+        per_row = 2.0 * n * n + n
+
+        def fn(rows):
+            oracle.gemm("f16", A, B, rows=rows % A.shape[0])
+            oracle.rowsum("f16", A, rows=rows % A.shape[0])
+        desc = "fp16 GEMM 65536 x 8192 x 8192 + row reduction"
+    elif name == "batched":
+        A = synth.uniform((64, 1024, 1024), synth.seed_for(2, 0))
+        B = synth.uniform((64, 1024, 1024), synth.seed_for(2, 1))
+        per_row = 2.0 * 1024 * 1024
+        m = 64 * 1024
+
+        def fn(rows):
+            for r in np.unique(rows // 1024):
+                oracle.gemm("f16", A[r], B[r], rows=rows[rows // 1024 == r] % 1024)
+        desc = "batched fp16 GEMM 64 x 1024^3"
+    elif name == "dual":
+        n = 8192
+        A = synth.uniform((n, n), synth.seed_for(3, 0))
+        B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
+        B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
+        per_row = 4.0 * n * n
+        m = n
+        fn = lambda rows: oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows)  # noqa: E731
+        desc = "dual-GEMM pair 8192^3"
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    nth = oracle.num_threads()
+    # size each step to ~2 s of CPU work so K + W steps end within a few minutes
+    probe = np.arange(max(nth, 4))
+    t0 = time.perf_counter()
+    fn(probe)
+    dt0 = time.perf_counter() - t0
+    rows_per_step = int(max(len(probe), min(m, len(probe) * 2.0 / max(dt0, 1e-3))))
+    steps = min(args.steps, 10)
+    warm = min(args.warmup, 3)
+    rng = np.random.default_rng(0)
+    for _ in range(warm):
+        fn(np.sort(rng.choice(m, rows_per_step, replace=False)))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fn(np.sort(rng.choice(m, rows_per_step, replace=False)))
+    dt = time.perf_counter() - t0
+    value = per_row * rows_per_step * steps / dt / 1e12
+    sample = f"{rows_per_step} random rows (all columns, full K) per step of {desc}; {steps} steps in {dt:.1f} s"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+           "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
+           "config": {"workload": desc, "parallelism": "CPU oracle, rank 0 only"},
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": nth, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -22,19 +23,19 @@ using cy::Params;
 // ------------------------------------------------------------------------------------------
 // kernel menu
 struct KDesc {
-  int var, dt, cg, bn, stages, threads, smem;
+  int var, dt, cg, bn, stages, threads, smem;  // bn = output tile width (TILE_N)
   const void* fn;
 };
 
-template <int DT, int CG, int BN, int ST, int VAR>
+template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1>
 KDesc kdesc() {
-  using C = cy::Cfg<DT, CG, BN, ST, VAR>;
-  return KDesc{VAR, DT, CG, BN, ST, C::THREADS, C::SMEM_BYTES, (const void*)&cy::cy_sm100_kernel<C>};
+  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB>;
+  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, (const void*)&cy::cy_sm100_kernel<C>};
 }
 
 // Shapes (cta_group, tile N) offered per variant; the GEMM menu defines the public config ids.
 struct Shape { int cg, bn; };
-constexpr Shape kGemmMenu[] = {{2, 256}, {2, 128}, {1, 256}, {1, 128}, {1, 64}};
+constexpr Shape kGemmMenu[] = {{2, 256}, {2, 128}, {1, 256}, {1, 128}, {1, 64}, {2, 512}};
 constexpr int kNumGemmCfg = sizeof(kGemmMenu) / sizeof(kGemmMenu[0]);
 
 template <int DT>
@@ -44,9 +45,11 @@ void add_all(std::vector<KDesc>& v) {
   v.push_back(kdesc<DT, 1, 256, 4, cy::V_GEMM>());
   v.push_back(kdesc<DT, 1, 128, 6, cy::V_GEMM>());
   v.push_back(kdesc<DT, 1, 64, 8, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2>());
   v.push_back(kdesc<DT, 2, 256, 6, cy::V_ROWREDUCE>());
   v.push_back(kdesc<DT, 2, 128, 8, cy::V_ROWREDUCE>());
   v.push_back(kdesc<DT, 1, 128, 6, cy::V_ROWREDUCE>());
+  v.push_back(kdesc<DT, 2, 256, 4, cy::V_ROWREDUCE, 2>());
   v.push_back(kdesc<DT, 2, 128, 6, cy::V_DUAL_PAIR>());
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_DUAL_PAIR>());
   v.push_back(kdesc<DT, 1, 128, 4, cy::V_DUAL_PAIR>());
@@ -66,6 +69,21 @@ const std::vector<KDesc>& menu() {
 }
 
 std::atomic<int> g_forced{-1};
+// CY_GROUP_M: rasterisation group width in m-blocks (tuning knob; default 8)
+const int g_group_m = [] {
+  const char* e = std::getenv("CY_GROUP_M");
+  return e ? std::atoi(e) : 0;
+}();
+// CY_L2_POLICY: TMA L2 eviction hints for A/B (tuning knob; see Params::l2_policy)
+const int g_l2_policy = [] {
+  const char* e = std::getenv("CY_L2_POLICY");
+  return e ? std::atoi(e) : 0;
+}();
+// CY_DEBUG_MODE: timing experiments only (invalid results); never set in production
+const int g_debug = [] {
+  const char* e = std::getenv("CY_DEBUG_MODE");
+  return e ? std::atoi(e) : 0;
+}();
 std::atomic<int> g_last{-1};
 std::atomic<int64_t> g_launches{0};
 
@@ -179,21 +197,25 @@ bool overlap(Range a, Range b) { return a.lo < a.hi && b.lo < b.hi && a.lo < b.h
 
 // ------------------------------------------------------------------------------------------
 // config choice: minimise (waves x tile area / efficiency)
-double cfg_cost(int cg, int bn, int64_t m, int64_t n, int64_t L, int sms) {
+double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k, int64_t L, int sms) {
+  // time ~ waves x (tile area per SM) x (K + exposed epilogue) / efficiency
   const int64_t bm = 128 * cg;
   const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
   const int64_t units = sms / cg;
   const int64_t waves = (tiles + units - 1) / units;
-  // relative per-SM tensor efficiency of each tile shape (shared-memory operand traffic per MMA)
+  // relative per-SM efficiency of each tile shape, measured on B200 at 8192^3 under the power cap
+  // (shared-memory operand bytes per MMA and L2 bytes per FLOP fall as the tile grows)
   double eff = 1.0;
-  if (cg == 2 && bn == 128) eff = 0.93;
-  if (cg == 1 && bn == 256) eff = 0.85;
-  if (cg == 1 && bn == 128) eff = 0.72;
-  if (cg == 1 && bn == 64) eff = 0.45;
-  return static_cast<double>(waves) * static_cast<double>(bm * bn) / cg / eff;
+  if (cg == 2 && bn == 512) eff = 1.06;
+  if (cg == 2 && bn == 128) eff = 0.70;
+  if (cg == 1 && bn == 256) eff = 0.80;
+  if (cg == 1 && bn == 128) eff = 0.60;
+  if (cg == 1 && bn == 64) eff = 0.40;
+  const double kk = static_cast<double>(std::max<int64_t>(k, 64)) + (single_buf ? 256.0 : 0.0) + 128.0;
+  return static_cast<double>(waves) * static_cast<double>(bm * bn) / cg * kk / eff;
 }
 
-int pick(int var, int dt, int64_t m, int64_t n, int64_t L, int sms) {
+int pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms) {
   const auto& mn = menu();
   int forced = g_forced.load();
   if (forced >= 0 && forced < kNumGemmCfg) {
@@ -206,8 +228,11 @@ int pick(int var, int dt, int64_t m, int64_t n, int64_t L, int sms) {
   double best_cost = 0;
   for (size_t i = 0; i < mn.size(); ++i) {
     if (mn[i].var != var || mn[i].dt != dt) continue;
-    double c = cfg_cost(mn[i].cg, mn[i].bn, m, n, L, sms);
-    if (var == cy::V_DUAL_PAIR && mn[i].bn == 256) c *= 1.04;  // single-buffered accumulators
+    const bool dual = (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM);
+    const int acc_cols = (var == cy::V_DUAL_PAIR ? 2 : 1) * (dual ? mn[i].bn : mn[i].bn);
+    const int single = acc_cols * 2 > 512;
+    double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, sms);
+    if (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM) c *= 1.0;
     if (best < 0 || c < best_cost) { best = static_cast<int>(i); best_cost = c; }
   }
   return best;
@@ -227,7 +252,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   cy_status_t s = device_state(dev, st);
   if (s != CY_OK) return s;
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX || L > INT32_MAX) return CY_ERR_INVALID_VALUE;
-  const int idx = pick(var, dt, m, n, L, st->sms);
+  const int idx = pick(var, dt, m, n, k, L, st->sms);
   if (idx < 0) return CY_ERR_INTERNAL;
   const KDesc& kd = menu()[idx];
   const int bm = 128 * kd.cg;
@@ -264,7 +289,9 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.n_blocks = (int)((n + kd.bn - 1) / kd.bn);
   p.k_blocks = (int)((k + 63) / 64);
   p.tiles = (int)(L * p.m_blocks * p.n_blocks);
-  p.group_m = 8;
+  p.group_m = g_group_m > 0 ? g_group_m : 8;
+  p.l2_policy = g_l2_policy;
+  p.debug = g_debug;
   p.y = y;
 
   {

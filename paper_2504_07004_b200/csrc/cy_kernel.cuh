@@ -41,24 +41,29 @@ struct Params {
   int m_blocks, n_blocks, k_blocks;
   int tiles;             // L * m_blocks * n_blocks
   int group_m;           // grouped rasterisation width (in m-blocks)
+  int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
+  int debug;             // timing experiments only (results invalid): 1 = no TMA refill, 2 = no epilogue
 };
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int DT_, int CG_, int BN_, int STAGES_, int VAR_>
+template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1>
 struct Cfg {
   static constexpr int DT = DT_;  // 0 = fp16, 1 = bf16
   static constexpr int CG = CG_;  // CTAs per MMA (tcgen05 cta_group)
-  static constexpr int BN = BN_;  // MMA N = output tile width
+  static constexpr int BN = BN_;  // MMA N (one accumulator's width)
   static constexpr int STAGES = STAGES_;
   static constexpr int VAR = VAR_;
+  static constexpr int NSUB = NSUB_;          // GEMM: N sub-tiles per tile sharing each A stage
+  static constexpr bool DUAL = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM);
   static constexpr int BM_CTA = 128;          // accumulator rows per CTA = TMEM lanes
   static constexpr int BM = BM_CTA * CG;      // MMA M = output tile height
+  static constexpr int TILE_N = DUAL ? BN : NSUB * BN;  // output tile width
   static constexpr int BK = 64;               // one 128-byte swizzle atom of K per stage
   static constexpr int UMMA_K = 16;
-  static constexpr int NUM_B = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM) ? 2 : 1;
-  static constexpr int NUM_ACC = (VAR == V_DUAL_PAIR) ? 2 : 1;
+  static constexpr int NUM_B = DUAL ? 2 : NSUB;  // B slots per stage
+  static constexpr int NUM_ACC = (VAR == V_DUAL_PAIR) ? 2 : (VAR == V_DUAL_SUM ? 1 : NSUB);
   static constexpr int BN_CTA = BN / CG;      // B columns held per CTA
   static constexpr int A_BYTES = BM_CTA * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
@@ -82,6 +87,7 @@ struct Cfg {
   static_assert(BN >= 64 && BN <= 256, "tcgen05 kind::f16 N range");
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static_assert(NUM_ACC_BUF * ACC_COLS <= 512, "TMEM has 512 columns");
+  static_assert(!DUAL || NSUB == 1, "dual GEMM uses its two B slots for B0/B1");
 
   // Instruction descriptor, kind::f16: c_format F32 [4,6) | a_format [7,10) | b_format [10,13) |
   // a_major K (bit 15 = 0) | b_major MN (bit 16 = 1) | N>>3 [17,23) | M>>4 [24,29).
@@ -153,9 +159,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB0);
-    if (C::NUM_B == 2) prefetch_tmap(&tmB1);
+    if (C::DUAL) prefetch_tmap(&tmB1);
     prefetch_tmap(&tmD0);
-    if (C::NUM_ACC == 2) prefetch_tmap(&tmD1);
+    if (C::VAR == V_DUAL_PAIR) prefetch_tmap(&tmD1);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -182,18 +188,31 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------------ producer (TMA)
     if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
+      uint64_t pol_a, pol_b;
+      switch (p.l2_policy) {
+        case 1: pol_a = pol_b = policy_evict_last(); break;
+        case 2: pol_a = pol_b = policy_evict_first(); break;
+        case 3: pol_a = policy_evict_first(); pol_b = policy_evict_last(); break;
+        case 4: pol_a = policy_evict_last(); pol_b = policy_evict_first(); break;
+        default: pol_a = pol_b = policy_evict_normal(); break;
+      }
+      const bool hint = p.l2_policy != 5;
       uint32_t stage = 0, phase = 0;
       constexpr bool PAIR_TMA = (C::CG == 2 && !C::RELAY);
       for (int t = cid; t < p.tiles; t += ncl) {
         int b, mb, nb;
         tile_coords(p, t, b, mb, nb);
         const int am = mb * C::BM + rank * C::BM_CTA;
-        const int bn = nb * C::BN + rank * C::BN_CTA;
+        const int bn = nb * C::TILE_N + rank * C::BN_CTA;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(bEmpty + 8 * stage, phase ^ 1);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
+          if ((p.debug & 1) && (phase || (t != cid))) {  // timing experiment: reuse stale stages
+            if (PAIR_TMA ? rank == 0 : true) mbar_arrive(fb);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if constexpr (PAIR_TMA) {
             if (rank == 0) mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
             fb = mapa(fb, 0);  // both CTAs count bytes on the leader's barrier
@@ -201,17 +220,24 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
           }
           const int k0 = kb * C::BK;
-          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1) {
-            if constexpr (PAIR_TMA) tma_load_3d_pair(dst, tm, fb, c0, c1, b, pol);
-            else tma_load_3d(dst, tm, fb, c0, c1, b, pol);
+          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint64_t pol) {
+            if constexpr (PAIR_TMA) {
+              if (hint) tma_load_3d_pair(dst, tm, fb, c0, c1, b, pol);
+              else tma_load_3d_pair_nohint(dst, tm, fb, c0, c1, b);
+            } else {
+              if (hint) tma_load_3d(dst, tm, fb, c0, c1, b, pol);
+              else tma_load_3d_nohint(dst, tm, fb, c0, c1, b);
+            }
           };
-          load(sA, &tmA, k0, am);
+          load(sA, &tmA, k0, am, pol_a);
 #pragma unroll
-          for (int j = 0; j < C::BN_CTA / 64; ++j) load(sA + C::A_BYTES + j * C::B_ATOM_BYTES, &tmB0, bn + 64 * j, k0);
-          if constexpr (C::NUM_B == 2) {
+          for (int sl = 0; sl < C::NUM_B; ++sl) {
+            // slot sl: dual -> B0 / B1 at the same columns; GEMM -> N sub-tile sl of B
+            const CUtensorMap* tmB = (C::DUAL && sl == 1) ? &tmB1 : &tmB0;
+            const int cb = bn + (C::DUAL ? 0 : sl * C::BN);
 #pragma unroll
             for (int j = 0; j < C::BN_CTA / 64; ++j)
-              load(sA + C::A_BYTES + C::B_BYTES + j * C::B_ATOM_BYTES, &tmB1, bn + 64 * j, k0);
+              load(sA + C::A_BYTES + sl * C::B_BYTES + j * C::B_ATOM_BYTES, tmB, cb + 64 * j, k0, pol_b);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -240,13 +266,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
             // B: MN-major SW128, 64-column atoms B_ATOM_BYTES apart (LBO), 8-K-row groups 1024 B
             // apart (SBO); K advances 16 rows = 2048 B.
-            const uint64_t bd = sdesc_sw128(sB0 + kk * 2048, C::B_ATOM_BYTES, 1024);
             const uint32_t acc = (kb | kk) != 0;
-            mma_f16<C::CG>(d, ad, bd, C::IDESC, acc);
-            if constexpr (C::NUM_B == 2) {
-              const uint64_t bd1 = sdesc_sw128(sB0 + C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
-              if constexpr (C::VAR == V_DUAL_PAIR) mma_f16<C::CG>(d + C::BN, ad, bd1, C::IDESC, acc);
-              else mma_f16<C::CG>(d, ad, bd1, C::IDESC, 1u);
+#pragma unroll
+            for (int sl = 0; sl < C::NUM_B; ++sl) {
+              const uint64_t bd = sdesc_sw128(sB0 + sl * C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
+              if constexpr (C::VAR == V_DUAL_SUM) mma_f16<C::CG>(d, ad, bd, C::IDESC, sl ? 1u : acc);
+              else mma_f16<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
             }
           }
           mma_commit<C::CG>(bEmpty + 8 * stage, 0x3);  // frees the stage in both CTAs
@@ -282,13 +307,23 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       mbar_wait(bTFull + 8 * buf, bph);
       tc_fence_after();
       const int row0 = mb * C::BM + rank * C::BM_CTA + 32 * q;
+      if (p.debug & 2) {  // timing experiment: drop the epilogue
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * buf, 0));
+          else mbar_arrive(bTEmpty + 8 * buf);
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int a = 0; a < C::NUM_ACC; ++a) {
-        const CUtensorMap* tmD = (a == 0) ? &tmD0 : &tmD1;
-        const CUtensorMap* tmC = (a == 0) ? &tmC0 : &tmC1;
+        const bool second = (C::VAR == V_DUAL_PAIR && a == 1);
+        const CUtensorMap* tmD = second ? &tmD1 : &tmD0;
+        const CUtensorMap* tmC = second ? &tmC1 : &tmC0;
 #pragma unroll 1
         for (int c = 0; c < C::BN / 64; ++c) {
-          const int n0 = nb * C::BN + 64 * c;
+          const int n0 = nb * C::TILE_N + (C::DUAL ? 0 : a * C::BN) + 64 * c;
           const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
           if (lane == 0) bulk_wait_read<1>();  // the store that last used this slot has read it
           __syncwarp();

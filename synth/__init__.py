@@ -50,10 +50,21 @@ def f64_to_bits(x: np.ndarray, dtype: str) -> np.ndarray:
     raise ValueError(dtype)
 
 
+_CHUNK = 1 << 24
+
+
 def uniform(shape, seed: int, dtype: str = "f16", lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
-    """uniform[lo, hi) drawn in float64, then cast to the 16-bit input format."""
-    x = _rng(seed).uniform(lo, hi, size=shape)
-    return f64_to_bits(x, dtype)
+    """uniform[lo, hi) drawn in float64, then cast to the 16-bit input format.
+    Large arrays are drawn in sequential chunks of one stream (same values as one draw)."""
+    rng = _rng(seed)
+    total = int(np.prod(shape))
+    if total <= _CHUNK:
+        return f64_to_bits(rng.uniform(lo, hi, size=shape), dtype)
+    out = np.empty(total, dtype=np.uint16)
+    for s in range(0, total, _CHUNK):
+        e = min(total, s + _CHUNK)
+        out[s:e] = f64_to_bits(rng.uniform(lo, hi, size=e - s), dtype)
+    return out.reshape(shape)
 
 
 def integers(shape, seed: int, dtype: str = "f16", lo: int = -2, hi: int = 2) -> np.ndarray:

@@ -181,7 +181,7 @@ def test_misaligned_ld_rejected():
 # ---------------------------------------------------------------- batched
 @pytest.mark.parametrize("cfg", ALL_CFGS)
 def test_batched_matches_oracle_and_slices(cfg):
-    L, m, n, k = 5, 300, 260, 200
+    L, m, n, k = 5, 300, 264, 200
     A, B, C = synth.gemm_inputs(m, n, k, seed=101, batch=L, with_c=True)
     cy.force_config(cfg)
     D = to_bits(cy.gemm_batched(to_dev(A, "f16"), to_dev(B, "f16"), to_dev(C, "f16"), 1.0, 1.0))
@@ -271,7 +271,7 @@ def test_rowreduce_integer_and_invariants():
     assert torch.equal(y, y2)
     # all-ones A: y = K exactly
     ones = torch.ones((256, 640), dtype=torch.float16, device="cuda")
-    _, y3 = cy.gemm_rowreduce(ones, torch.zeros((640, n), dtype=torch.float16, device="cuda"))
+    _, y3 = cy.gemm_rowreduce(ones, torch.zeros((640, 304), dtype=torch.float16, device="cuda"))
     assert (y3 == 640.0).all()
 
 
