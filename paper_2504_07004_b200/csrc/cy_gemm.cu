@@ -84,6 +84,11 @@ const int g_debug = [] {
   const char* e = std::getenv("CY_DEBUG_MODE");
   return e ? std::atoi(e) : 0;
 }();
+// CY_SCHED: 0 = dynamic (cluster launch control) when there is more than one wave, 1 = static
+const int g_sched = [] {
+  const char* e = std::getenv("CY_SCHED");
+  return e ? std::atoi(e) : 0;
+}();
 std::atomic<int> g_last{-1};
 std::atomic<int64_t> g_launches{0};
 
@@ -306,7 +311,11 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
     }
   }
   const int units = std::max(1, st->sms / kd.cg);
-  const int clusters = std::max(1, std::min(p.tiles, units));
+  // More tiles than co-resident clusters: launch one cluster per tile and let running clusters
+  // steal pending ones (cluster launch control) so the tiles in flight stay adjacent in the
+  // raster; otherwise every tile gets its own resident cluster.
+  p.dyn = (p.tiles > units && g_sched != 1) ? 1 : 0;
+  const int clusters = p.dyn ? p.tiles : std::max(1, std::min(p.tiles, units));
 
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));

@@ -44,6 +44,8 @@ struct Params {
   int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
   int debug;             // timing experiments only (results invalid): 1 = no TMA refill, 2 = no epilogue
+  int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
+                         //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride
 };
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
@@ -78,6 +80,8 @@ struct Cfg {
   static constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 64 columns x 2 B
   static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;
   static constexpr int BAR_BYTES = 512;
+  static constexpr int SCHED_SLOTS = 4;       // tile-ID ring depth (dynamic schedule)
+  static constexpr int NUM_WARPS = THREADS / 32;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   // Row-reduce with CTA pairs: each CTA counts its own TMA bytes on its own full barrier (the
   // reducer warps must see their local A stage land); the peer relays "full" to the leader.
@@ -148,6 +152,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const uint32_t bTEmpty = bTFull + 16;                      // [2]
   const uint32_t bCBar = bTFull + 32;                        // [4]: per-epilogue-warp C-tile loads
   const uint32_t sTmemSlot = bTFull + 64;
+  const uint32_t bSFull = bTFull + 72;                       // [SCHED_SLOTS] tile-ID ring: response landed
+  const uint32_t bSEmpty = bSFull + 8 * C::SCHED_SLOTS;      // [SCHED_SLOTS] all warps of the cluster read it
+  const uint32_t sResp = (bSEmpty + 8 * C::SCHED_SLOTS + 15u) & ~15u;  // [SCHED_SLOTS] x 16-B responses
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5;
@@ -174,6 +181,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       mbar_init(bTEmpty + 8 * b, C::CG * C::EPI_WARPS);
     }
     for (int w = 0; w < 4; ++w) mbar_init(bCBar + 8 * w, 1);
+    for (int j = 0; j < C::SCHED_SLOTS; ++j) {
+      mbar_init(bSFull + 8 * j, 1);
+      mbar_init(bSEmpty + 8 * j, C::CG * C::NUM_WARPS);
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -184,6 +195,45 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if constexpr (C::CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  // ---------------------------------------------------------------- tile schedule
+  // Tile i of this cluster: static -> cid + i*ncl; dynamic -> i == 0: own cluster's tile, i > 0:
+  // the tile of the cluster that try_cancel stole for us (ring slot (i-1) % SCHED_SLOTS).
+  // Every warp of both CTAs reads every slot and releases it on the leader's bSEmpty.
+  auto sched_next = [&](int i, int& t, bool warp_wide) -> bool {
+    if (!p.dyn) {
+      t = cid + i * ncl;
+      return t < p.tiles;
+    }
+    if (i == 0) {
+      t = cid;
+      return t < p.tiles;
+    }
+    const int j = (i - 1) % C::SCHED_SLOTS;
+    const uint32_t ph = ((i - 1) / C::SCHED_SLOTS) & 1;
+    mbar_wait(bSFull + 8 * j, ph);
+    uint32_t ok, cx;
+    clc_decode(sResp + 16 * j, ok, cx);
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane == 0) {
+      if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bSEmpty + 8 * j, 0));
+      else mbar_arrive(bSEmpty + 8 * j);
+    }
+    t = static_cast<int>(cx) / C::CG;
+    return ok != 0;
+  };
+  // Producer thread, at the start of its tile i: arm this CTA's slot for tile i+1 and (leader)
+  // ask the hardware for the next pending cluster.
+  auto sched_request = [&](int i) {
+    if (!p.dyn) return;
+    const int j = i % C::SCHED_SLOTS;
+    mbar_arrive_expect_tx(bSFull + 8 * j, 16);
+    if (rank == 0) {
+      mbar_wait(bSEmpty + 8 * j, ((i / C::SCHED_SLOTS) & 1) ^ 1);
+      if constexpr (C::CG == 2) clc_try_cancel_multicast(sResp + 16 * j, bSFull + 8 * j);
+      else clc_try_cancel(sResp + 16 * j, bSFull + 8 * j);
+    }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer (TMA)
@@ -199,7 +249,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const bool hint = p.l2_policy != 5;
       uint32_t stage = 0, phase = 0;
       constexpr bool PAIR_TMA = (C::CG == 2 && !C::RELAY);
-      for (int t = cid; t < p.tiles; t += ncl) {
+      int t;
+      for (int i = 0; sched_next(i, t, false); ++i) {
+        sched_request(i);
         int b, mb, nb;
         tile_coords(p, t, b, mb, nb);
         const int am = mb * C::BM + rank * C::BM_CTA;
@@ -208,7 +260,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           mbar_wait(bEmpty + 8 * stage, phase ^ 1);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
-          if ((p.debug & 1) && (phase || (t != cid))) {  // timing experiment: reuse stale stages
+          if ((p.debug & 1) && (phase || i != 0)) {  // timing experiment: reuse stale stages
             if (PAIR_TMA ? rank == 0 : true) mbar_arrive(fb);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             continue;
@@ -247,8 +299,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0;
-      int it = 0;
-      for (int t = cid; t < p.tiles; t += ncl, ++it) {
+      int t;
+      for (int it = 0; sched_next(it, t, false); ++it) {
         const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
         const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
@@ -279,16 +331,21 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
         mma_commit<C::CG>(bTFull + 8 * buf, 0x3);      // accumulator ready, both CTAs
       }
-    } else if (C::RELAY && lane == 0 && rank == 1) {
-      // peer CTA: relay "my stage landed" to the leader's second full barrier
+    } else if (lane == 0) {
+      // peer CTA: follow the tile schedule; with RELAY, relay "my stage landed" to the leader's
+      // second full barrier
       uint32_t stage = 0, phase = 0;
       const uint32_t pf0 = mapa(bPFull, 0);
-      for (int t = cid; t < p.tiles; t += ncl)
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(bFull + 8 * stage, phase);
-          mbar_arrive_cluster(pf0 + 8 * stage);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      int t;
+      for (int it = 0; sched_next(it, t, false); ++it) {
+        if constexpr (C::RELAY) {
+          for (int kb = 0; kb < p.k_blocks; ++kb) {
+            mbar_wait(bFull + 8 * stage, phase);
+            mbar_arrive_cluster(pf0 + 8 * stage);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
         }
+      }
     }
   } else if (warp < 2 + C::EPI_WARPS) {
     // ------------------------------------------------------------------ epilogue
@@ -298,8 +355,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     const uint32_t cbar = bCBar + 8 * ew;
     const uint64_t pol = policy_evict_normal();
     uint32_t slot = 0, cphase = 0;
-    int it = 0;
-    for (int t = cid; t < p.tiles; t += ncl, ++it) {
+    int t;
+    for (int it = 0; sched_next(it, t, true); ++it) {
       int b, mb, nb;
       tile_coords(p, t, b, mb, nb);
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
@@ -391,7 +448,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     const int q = warp & 3;
     const int r = 32 * q + lane;  // row of this CTA's 128-row A stage
     uint32_t stage = 0, phase = 0;
-    for (int t = cid; t < p.tiles; t += ncl) {
+    int t;
+    for (int it = 0; sched_next(it, t, true); ++it) {
       int b, mb, nb;
       tile_coords(p, t, b, mb, nb);
       const bool do_red = (nb == 0);  // one n-tile per row block reduces: no atomics, deterministic
