@@ -148,6 +148,20 @@ std::mutex g_map_mu;
 std::vector<MapEntry> g_maps;
 uint64_t g_tick = 0;
 
+// CY_L2_PROMO: TMA L2 sector promotion (tuning knob): 0 none, 1 64B, 2 128B, 3 256B (default)
+CUtensorMapL2promotion promo() {
+  static const int v = [] {
+    const char* e = std::getenv("CY_L2_PROMO");
+    return e ? std::atoi(e) : 3;
+  }();
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64_t rows, uint64_t batch,
                 uint64_t ld, uint64_t stride, uint32_t box_c, uint32_t box_r) {
   MapKey key;
@@ -170,7 +184,7 @@ bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64
   CUtensorMap m;
   CUresult r = g_encode(&m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                         const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_128B, promo(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   *out = m;

@@ -83,9 +83,13 @@ struct Cfg {
   static constexpr int SCHED_SLOTS = 4;       // tile-ID ring depth (dynamic schedule)
   static constexpr int NUM_WARPS = THREADS / 32;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
-  // Row-reduce with CTA pairs: each CTA counts its own TMA bytes on its own full barrier (the
-  // reducer warps must see their local A stage land); the peer relays "full" to the leader.
-  static constexpr bool RELAY = (CG == 2 && VAR == V_ROWREDUCE);
+  // Row-reduce: the reducer warps learn that their CTA's A stage is in shared memory from a
+  // second tcgen05.commit (bMDone, multicast to both CTAs of a pair) issued after the MMAs that
+  // read the stage; the stage is released only when the MMAs and the reducers are both done.
+  static constexpr bool REDUCE = (VAR == V_ROWREDUCE);
+  // Single-buffered TMEM with two accumulators: the epilogue releases them one at a time and the
+  // MMA issuer starts the next tile on accumulator 0 while accumulator 1 drains.
+  static constexpr bool SPLIT = (NUM_ACC_BUF == 1 && NUM_ACC == 2);
 
   static_assert(BN % 64 == 0 && BN_CTA % 64 == 0, "B is loaded in 64-column swizzle atoms");
   static_assert(BN >= 64 && BN <= 256, "tcgen05 kind::f16 N range");
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const uint32_t sBar = sEpi + C::EPI_BYTES;
   const uint32_t bFull = sBar;                               // [STAGES]
   const uint32_t bEmpty = sBar + 8 * C::STAGES;              // [STAGES]
-  const uint32_t bPFull = sBar + 16 * C::STAGES;             // [STAGES] (RELAY only)
+  const uint32_t bMDone = sBar + 16 * C::STAGES;             // [STAGES] (REDUCE only): MMAs read it
   const uint32_t bTFull = sBar + 24 * C::STAGES;             // [2]
   const uint32_t bTEmpty = bTFull + 16;                      // [2]
   const uint32_t bCBar = bTFull + 32;                        // [4]: per-epilogue-warp C-tile loads
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(bFull + 8 * s, 1);
       mbar_init(bEmpty + 8 * s, 1 + C::RED_WARPS);
-      if (C::RELAY) mbar_init(bPFull + 8 * s, 1);
+      if (C::REDUCE) mbar_init(bMDone + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bTFull + 8 * b, 1);
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
       const bool hint = p.l2_policy != 5;
       uint32_t stage = 0, phase = 0;
-      constexpr bool PAIR_TMA = (C::CG == 2 && !C::RELAY);
+      constexpr bool PAIR_TMA = (C::CG == 2);
       int t;
       for (int i = 0; sched_next(i, t, false); ++i) {
         sched_request(i);
@@ -299,52 +303,88 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0;
+      // all 4 k16 MMAs of one k-block for B slot `sl` of ring stage `st` into accumulator base `d`
+      auto issue = [&](uint32_t d, int st, int sl, int kb) {
+        const uint32_t sA = sStage0 + st * C::STAGE_BYTES;
+        const uint32_t sB = sA + C::A_BYTES + sl * C::B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
+          // A: K-major SW128, 8-row groups 1024 B apart; K advances 32 B inside the atom.
+          const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
+          // B: MN-major SW128, 64-column atoms B_ATOM_BYTES apart (LBO), 8-K-row groups 1024 B
+          // apart (SBO); K advances 16 rows = 2048 B.
+          const uint64_t bd = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
+          const uint32_t acc = (kb | kk) != 0;
+          if constexpr (C::VAR == V_DUAL_SUM) mma_f16<C::CG>(d, ad, bd, C::IDESC, sl ? 1u : acc);
+          else mma_f16<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
+        }
+      };
+      auto release = [&](int st) {
+        mma_commit<C::CG>(bEmpty + 8 * st, 0x3);  // frees the stage in both CTAs
+        if constexpr (C::REDUCE) mma_commit<C::CG>(bMDone + 8 * st, 0x3);  // reducers may read it
+      };
       int t;
       for (int it = 0; sched_next(it, t, false); ++it) {
         const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
         const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
-        mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
-        tc_fence_after();
         const uint32_t d = tmem_base + buf * C::ACC_COLS;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(bFull + 8 * stage, phase);
-          if constexpr (C::RELAY) mbar_wait(bPFull + 8 * stage, phase);
+        if constexpr (!C::SPLIT) {
+          mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
           tc_fence_after();
-          const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
-          const uint32_t sB0 = sA + C::A_BYTES;
+          for (int kb = 0; kb < p.k_blocks; ++kb) {
+            mbar_wait(bFull + 8 * stage, phase);
+            tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
-            // A: K-major SW128, 8-row groups 1024 B apart; K advances 32 B inside the atom.
-            const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
-            // B: MN-major SW128, 64-column atoms B_ATOM_BYTES apart (LBO), 8-K-row groups 1024 B
-            // apart (SBO); K advances 16 rows = 2048 B.
-            const uint32_t acc = (kb | kk) != 0;
-#pragma unroll
-            for (int sl = 0; sl < C::NUM_B; ++sl) {
-              const uint64_t bd = sdesc_sw128(sB0 + sl * C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
-              if constexpr (C::VAR == V_DUAL_SUM) mma_f16<C::CG>(d, ad, bd, C::IDESC, sl ? 1u : acc);
-              else mma_f16<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
-            }
+            for (int sl = 0; sl < C::NUM_B; ++sl) issue(d, stage, sl, kb);
+            release(stage);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit<C::CG>(bEmpty + 8 * stage, 0x3);  // frees the stage in both CTAs
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        } else {
+          // bTEmpty[a] = accumulator a drained by both CTAs' epilogues
+          mbar_wait(bTEmpty, bph ^ 1);
+          tc_fence_after();
+          bool acc1 = false;
+          int held = 0, held0 = 0, held_kb0 = 0;
+          auto flush = [&]() {  // accumulator-1 MMAs of the held stages, in k order, then release
+            for (int h = 0; h < held; ++h) {
+              const int st = (held0 + h) % C::STAGES;
+              issue(d, st, 1, held_kb0 + h);
+              release(st);
+            }
+            held = 0;
+          };
+          for (int kb = 0; kb < p.k_blocks; ++kb) {
+            mbar_wait(bFull + 8 * stage, phase);
+            tc_fence_after();
+            issue(d, stage, 0, kb);
+            if (!acc1 && mbar_test_wait(bTEmpty + 8, bph ^ 1)) {
+              acc1 = true;
+              tc_fence_after();
+            }
+            if (held == 0) { held0 = stage; held_kb0 = kb; }
+            ++held;
+            if (acc1) {
+              flush();
+            } else if (held == C::STAGES) {  // every stage is held: wait for accumulator 1
+              mbar_wait(bTEmpty + 8, bph ^ 1);
+              acc1 = true;
+              tc_fence_after();
+              flush();
+            }
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          if (held) {
+            mbar_wait(bTEmpty + 8, bph ^ 1);
+            tc_fence_after();
+            flush();
+          }
         }
         mma_commit<C::CG>(bTFull + 8 * buf, 0x3);      // accumulator ready, both CTAs
       }
     } else if (lane == 0) {
-      // peer CTA: follow the tile schedule; with RELAY, relay "my stage landed" to the leader's
-      // second full barrier
-      uint32_t stage = 0, phase = 0;
-      const uint32_t pf0 = mapa(bPFull, 0);
+      // peer CTA: the leader issues all MMAs; follow the tile schedule only
       int t;
       for (int it = 0; sched_next(it, t, false); ++it) {
-        if constexpr (C::RELAY) {
-          for (int kb = 0; kb < p.k_blocks; ++kb) {
-            mbar_wait(bFull + 8 * stage, phase);
-            mbar_arrive_cluster(pf0 + 8 * stage);
-            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-          }
-        }
       }
     }
   } else if (warp < 2 + C::EPI_WARPS) {
@@ -368,8 +408,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * buf, 0));
-          else mbar_arrive(bTEmpty + 8 * buf);
+          for (int a = 0; a < (C::SPLIT ? 2 : 1); ++a) {
+            const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
+            if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, 0));
+            else mbar_arrive(bar);
+          }
         }
         continue;
       }
@@ -433,13 +476,23 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           }
           slot ^= 1;
         }
+        if constexpr (C::SPLIT) {  // accumulator a drained: the next tile may start writing it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * a, 0));
+            else mbar_arrive(bTEmpty + 8 * a);
+          }
+        }
       }
-      // every tcgen05.ld of this accumulator buffer has completed (wait::ld above)
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * buf, 0));
-        else mbar_arrive(bTEmpty + 8 * buf);
+      if constexpr (!C::SPLIT) {
+        // every tcgen05.ld of this accumulator buffer has completed (wait::ld above)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * buf, 0));
+          else mbar_arrive(bTEmpty + 8 * buf);
+        }
       }
     }
     if (lane == 0) bulk_wait<0>();
@@ -455,7 +508,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const bool do_red = (nb == 0);  // one n-tile per row block reduces: no atomics, deterministic
       float acc = 0.f;
       for (int kb = 0; kb < p.k_blocks; ++kb) {
-        mbar_wait(bFull + 8 * stage, phase);
+        mbar_wait(bMDone + 8 * stage, phase);  // the tensor core has read this stage; it is still resident
         if (do_red) {
           const uint32_t row_addr = sStage0 + stage * C::STAGE_BYTES + r * 128;
 #pragma unroll
