@@ -67,10 +67,11 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
-def _stream(stream):
-    torch = _torch()
+def _stream(stream, like=None):
     if stream is None:
-        return torch.cuda.current_stream().cuda_stream
+        torch = _torch()
+        dev = like.device.index if like is not None and like.device.index is not None else torch.cuda.current_device()
+        return torch._C._cuda_getCurrentRawStream(dev)
     return getattr(stream, "cuda_stream", stream)
 
 
@@ -93,7 +94,7 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=N
     lib = _lib.load()
     st = lib.cy_gemm(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
                      _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n,
-                     _ptr(out), _ld(out, "out"), _stream(stream))
+                     _ptr(out), _ld(out, "out"), _stream(stream, A))
     check(st, "cy_gemm")
     return out
 
@@ -120,7 +121,7 @@ def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, 
     ldd, sd = lds(out)
     st = _lib.load().cy_gemm_batched(_dt(A), m, n, k, L, float(alpha), _ptr(A), lda, sa, _ptr(B), ldb, sb,
                                      float(beta), _ptr(C) if beta != 0 else None, ldc, sc, _ptr(out), ldd, sd,
-                                     _stream(stream))
+                                     _stream(stream, A))
     check(st, "cy_gemm_batched")
     return out
 
@@ -146,7 +147,7 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
         _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), float(beta), _ptr(C0) if use_c else None,
         _ld(C0, "C0") if (use_c and C0 is not None) else n, _ptr(C1) if (use_c and pair) else None,
         _ld(C1, "C1") if (use_c and pair and C1 is not None) else n, _ptr(out0), _ld(out0, "out0"),
-        _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream))
+        _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, A))
     check(st, "cy_dual_gemm")
     return (out0, out1) if pair else out0
 
@@ -164,7 +165,7 @@ def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None
     st = _lib.load().cy_gemm_rowreduce(
         _dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
         _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n, _ptr(out),
-        _ld(out, "out"), _ptr(y), _stream(stream))
+        _ld(out, "out"), _ptr(y), _stream(stream, A))
     check(st, "cy_gemm_rowreduce")
     return out, y
 

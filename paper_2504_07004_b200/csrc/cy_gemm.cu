@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "cy_kernel.cuh"
@@ -132,22 +133,6 @@ cy_status_t device_state(int& dev, DevState*& st) {
 
 // ------------------------------------------------------------------------------------------
 // TMA descriptors (3-D: columns, rows, batch), cached
-struct MapKey {
-  const void* ptr;
-  uint64_t cols, rows, batch, ld, stride;
-  uint32_t box_c, box_r;
-  int dt;
-  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
-};
-struct MapEntry {
-  MapKey key;
-  CUtensorMap map;
-  uint64_t tick;
-};
-std::mutex g_map_mu;
-std::vector<MapEntry> g_maps;
-uint64_t g_tick = 0;
-
 // CY_L2_PROMO: TMA L2 sector promotion (tuning knob): 0 none, 1 64B, 2 128B, 3 256B (default)
 CUtensorMapL2promotion promo() {
   static const int v = [] {
@@ -162,6 +147,25 @@ CUtensorMapL2promotion promo() {
   }
 }
 
+struct MapKey {
+  const void* ptr;
+  uint64_t cols, rows, batch, ld, stride;
+  uint32_t box_c, box_r;
+  int dt, pad;
+  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    // FNV-1a over the key bytes
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&k);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof(MapKey); ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return static_cast<size_t>(h);
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;  // bounded: cleared when it grows past 4096
+
 bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64_t rows, uint64_t batch,
                 uint64_t ld, uint64_t stride, uint32_t box_c, uint32_t box_r) {
   MapKey key;
@@ -170,12 +174,11 @@ bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64
   key.box_c = box_c; key.box_r = box_r; key.dt = dt;
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
-    for (auto& e : g_maps)
-      if (e.key == key) {
-        e.tick = ++g_tick;
-        *out = e.map;
-        return true;
-      }
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return true;
+    }
   }
   cuuint64_t dims[3] = {cols, rows, batch};
   cuuint64_t strides[2] = {ld * 2, stride * 2};
@@ -184,18 +187,12 @@ bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64
   CUtensorMap m;
   CUresult r = g_encode(&m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                         const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, promo(),
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_SWIZZLE_128B, promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   *out = m;
   std::lock_guard<std::mutex> lk(g_map_mu);
-  if (g_maps.size() < 256) {
-    g_maps.push_back(MapEntry{key, m, ++g_tick});
-  } else {
-    auto lru = std::min_element(g_maps.begin(), g_maps.end(),
-                                [](const MapEntry& a, const MapEntry& b) { return a.tick < b.tick; });
-    *lru = MapEntry{key, m, ++g_tick};
-  }
+  if (g_maps.size() >= 4096) g_maps.clear();
+  g_maps.emplace(key, m);
   return true;
 }
 

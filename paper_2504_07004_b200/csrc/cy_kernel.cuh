@@ -74,11 +74,15 @@ struct Cfg {
   static constexpr int ACC_COLS = NUM_ACC * BN;
   static constexpr int NUM_ACC_BUF = (2 * ACC_COLS <= 512) ? 2 : 1;
   static constexpr int TMEM_COLS = pow2_cols(NUM_ACC_BUF * ACC_COLS);
-  static constexpr int EPI_WARPS = 4;
+  // Single-buffered accumulators (TMEM full) leave the epilogue exposed: give it two warps per
+  // TMEM lane quarter (each takes every other 64-column chunk) and one staging buffer each.
+  static constexpr int EPI_SPLIT = (NUM_ACC_BUF == 1) ? 2 : 1;
+  static constexpr int EPI_WARPS = 4 * EPI_SPLIT;
+  static constexpr int EPI_BUFS = (EPI_SPLIT == 2) ? 1 : 2;
   static constexpr int RED_WARPS = (VAR == V_ROWREDUCE) ? 4 : 0;
   static constexpr int THREADS = 32 * (2 + EPI_WARPS + RED_WARPS);
   static constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 64 columns x 2 B
-  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;
+  static constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
   static constexpr int BAR_BYTES = 512;
   static constexpr int SCHED_SLOTS = 4;       // tile-ID ring depth (dynamic schedule)
   static constexpr int NUM_WARPS = THREADS / 32;
@@ -154,9 +158,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const uint32_t bMDone = sBar + 16 * C::STAGES;             // [STAGES] (REDUCE only): MMAs read it
   const uint32_t bTFull = sBar + 24 * C::STAGES;             // [2]
   const uint32_t bTEmpty = bTFull + 16;                      // [2]
-  const uint32_t bCBar = bTFull + 32;                        // [4]: per-epilogue-warp C-tile loads
-  const uint32_t sTmemSlot = bTFull + 64;
-  const uint32_t bSFull = bTFull + 72;                       // [SCHED_SLOTS] tile-ID ring: response landed
+  const uint32_t bCBar = bTFull + 32;                        // [8]: per-epilogue-warp C-tile loads
+  const uint32_t sTmemSlot = bTFull + 96;
+  const uint32_t bSFull = bTFull + 104;                      // [SCHED_SLOTS] tile-ID ring: response landed
   const uint32_t bSEmpty = bSFull + 8 * C::SCHED_SLOTS;      // [SCHED_SLOTS] all warps of the cluster read it
   const uint32_t sResp = (bSEmpty + 8 * C::SCHED_SLOTS + 15u) & ~15u;  // [SCHED_SLOTS] x 16-B responses
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       mbar_init(bTFull + 8 * b, 1);
       mbar_init(bTEmpty + 8 * b, C::CG * C::EPI_WARPS);
     }
-    for (int w = 0; w < 4; ++w) mbar_init(bCBar + 8 * w, 1);
+    for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(bCBar + 8 * w, 1);
     for (int j = 0; j < C::SCHED_SLOTS; ++j) {
       mbar_init(bSFull + 8 * j, 1);
       mbar_init(bSEmpty + 8 * j, C::CG * C::NUM_WARPS);
@@ -391,7 +395,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     // ------------------------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const uint32_t sE = sEpi + ew * 2 * C::EPI_BUF_BYTES;
+    const int half = ew / 4;  // EPI_SPLIT == 2: this warp takes chunks c with c % 2 == half
+    const uint32_t sE = sEpi + ew * C::EPI_BUFS * C::EPI_BUF_BYTES;
     const uint32_t cbar = bCBar + 8 * ew;
     const uint64_t pol = policy_evict_normal();
     uint32_t slot = 0, cphase = 0;
@@ -422,10 +427,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const CUtensorMap* tmD = second ? &tmD1 : &tmD0;
         const CUtensorMap* tmC = second ? &tmC1 : &tmC0;
 #pragma unroll 1
-        for (int c = 0; c < C::BN / 64; ++c) {
+        for (int c = (C::EPI_SPLIT == 2 ? half : 0); c < C::BN / 64; c += C::EPI_SPLIT) {
           const int n0 = nb * C::TILE_N + (C::DUAL ? 0 : a * C::BN) + 64 * c;
           const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
-          if (lane == 0) bulk_wait_read<1>();  // the store that last used this slot has read it
+          if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // the store that last used this slot has read it
           __syncwarp();
           if (p.has_c) {
             if (lane == 0) {
@@ -445,7 +450,20 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) r0[i] = r1[i] = 0u;
           }
+          // The last chunk of this accumulator (buffer) is in registers: hand the TMEM columns back
+          // to the MMA issuer before converting and storing it.
+          if (c + C::EPI_SPLIT >= C::BN / 64 && (C::SPLIT || a == C::NUM_ACC - 1)) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
+              if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, 0));
+              else mbar_arrive(bar);
+            }
+          }
+          if (p.debug & 8) continue;  // timing experiment: TMEM loads only
           const uint32_t row_addr = sb + lane * 128;
+          const bool unit_alpha = (p.alpha == 1.0f);
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
             const uint32_t addr = row_addr + ((v ^ (lane & 7)) << 4);  // SWIZZLE_128B chunk
@@ -453,7 +471,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int col = 8 * v + e;
-              f[e] = __uint_as_float(col < 32 ? r0[col] : r1[col - 32]) * p.alpha;
+              const float x = __uint_as_float(col < 32 ? r0[col] : r1[col - 32]);
+              f[e] = unit_alpha ? x : x * p.alpha;
             }
             if (p.has_c) {
               uint32_t cv[4];
@@ -470,28 +489,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(p.debug & 4)) {  // (debug 4: timing experiment without the D stores)
             tma_store_3d(tmD, sb, n0, row0, b);
             bulk_commit();
           }
-          slot ^= 1;
-        }
-        if constexpr (C::SPLIT) {  // accumulator a drained: the next tile may start writing it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * a, 0));
-            else mbar_arrive(bTEmpty + 8 * a);
-          }
-        }
-      }
-      if constexpr (!C::SPLIT) {
-        // every tcgen05.ld of this accumulator buffer has completed (wait::ld above)
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bTEmpty + 8 * buf, 0));
-          else mbar_arrive(bTEmpty + 8 * buf);
+          if constexpr (C::EPI_BUFS == 2) slot ^= 1;
         }
       }
     }

@@ -51,9 +51,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// Arrive on a barrier given by its shared::cluster address (possibly in the peer CTA).
+// Arrive on a barrier given by its shared::cluster address (possibly in the peer CTA).  Default
+// (.release.cta) semantics: the callers order their tensor-memory reads with tcgen05 fences and
+// need no GPU-scope fence (the .release.cluster form compiles to MEMBAR.ALL.GPU, which waits for
+// this thread's in-flight global stores).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
