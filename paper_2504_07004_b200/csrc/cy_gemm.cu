@@ -90,6 +90,11 @@ const int g_sched = [] {
   const char* e = std::getenv("CY_SCHED");
   return e ? std::atoi(e) : 0;
 }();
+// CY_PDL=0 disables programmatic dependent launch (tuning / debugging knob)
+const int g_pdl = [] {
+  const char* e = std::getenv("CY_PDL");
+  return e ? std::atoi(e) : 1;
+}();
 std::atomic<int> g_last{-1};
 std::atomic<int64_t> g_launches{0};
 
@@ -334,13 +339,17 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   cfg.blockDim = dim3(kd.threads, 1, 1);
   cfg.dynamicSmemBytes = kd.smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = kd.cg;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
+  // Programmatic dependent launch: our prologue may overlap the previous kernel's tail; the
+  // kernel waits (griddepcontrol.wait) before its first global-memory access.
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   void* args[] = {&tA, &tB0, &tB1, &tC0, &tC1, &tD0, &tD1, &p};
   cudaError_t e = cudaLaunchKernelExC(&cfg, kd.fn, args);
   if (e != cudaSuccess) {

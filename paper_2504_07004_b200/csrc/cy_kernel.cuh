@@ -203,6 +203,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if constexpr (C::CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Everything above (barrier init, TMEM allocation, descriptor prefetch) overlapped the tail of
+  // the previous kernel on this stream; global memory is touched only after it has completed.
+  pdl_wait();
+  if (threadIdx.x == 0) pdl_launch_dependents();
 
   // ---------------------------------------------------------------- tile schedule
   // Tile i of this cluster: static -> cid + i*ncl; dynamic -> i == 0: own cluster's tile, i > 0:
@@ -497,7 +501,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // shared staging must outlive the stores' reads
   } else {
     // ------------------------------------------------------------------ row reduction (SIMT)
     const int q = warp & 3;
