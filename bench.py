@@ -359,20 +359,33 @@ def main():
         for i in range(warmup):
             fn(i)
         barrier()
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        # per-step events only when steps are long enough that recording them costs nothing
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn(warmup)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        per_step = e0.elapsed_time(e1) > 0.2
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps if per_step else 1)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps if per_step else 1)]
         n0 = cy.launch_count()
         sampler = ClockSampler(local)
         with sampler:
             barrier()
-            for i in range(steps):
-                starts[i].record(stream)
-                fn(warmup + i)
-                ends[i].record(stream)
+            if per_step:
+                for i in range(steps):
+                    starts[i].record(stream)
+                    fn(warmup + 1 + i)
+                    ends[i].record(stream)
+            else:
+                starts[0].record(stream)
+                for i in range(steps):
+                    fn(warmup + 1 + i)
+                ends[0].record(stream)
             barrier()
         launches = cy.launch_count() - n0
         total_ms = starts[0].elapsed_time(ends[-1])
-        per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        per = [s.elapsed_time(e) for s, e in zip(starts, ends)] if per_step else [total_ms / steps]
         return total_ms, per, launches, sampler
 
     attempts = 0

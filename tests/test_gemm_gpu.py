@@ -299,3 +299,62 @@ def test_full_rowreduce_65536_sampled():
     assert_within_tol(D_s, ref, k, "f16", what="65536 rowreduce D")
     yref = oracle.rowsum("f16", A, rows=rows)
     assert (np.abs(y.cpu().numpy()[rows] - yref) <= oracle.tolerance(yref, k)).all()
+
+
+# ---------------------------------------------------------------- more coverage: dynamic schedule, bf16, long K
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+def test_ragged_multiwave_dynamic_schedule(cfg):
+    """Ragged shape with more tiles than co-resident clusters (cluster-launch-control schedule)."""
+    m, n, k = 3000, 5000, 392
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=141 + cfg, kind="int")
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16", cfg)
+    rows = synth.sample_rows(m, n_random=32)
+    assert_bits_equal(D[rows], oracle.encode("f16", oracle.gemm("f16", A, B, rows=rows)), f"cfg{cfg}")
+
+
+@pytest.mark.parametrize("mode", ["pair", "sum"])
+def test_dual_bf16(mode):
+    m, n, k = 520, 392, 264
+    A, B0, B1, C0, C1 = synth.dual_inputs(m, n, k, seed=151, dtype="bf16", with_c=True)
+    d = cy.dual_gemm(*(to_dev(x, "bf16") for x in (A, B0, B1, C0, C1 if mode == "pair" else None)),
+                     alpha=1.25, beta=0.5, mode=mode) if mode == "pair" else \
+        cy.dual_gemm(to_dev(A, "bf16"), to_dev(B0, "bf16"), to_dev(B1, "bf16"), to_dev(C0, "bf16"),
+                     alpha=1.25, beta=0.5, mode="sum")
+    ref = oracle.dual_gemm("bf16", mode, A, B0, B1, C0, C1 if mode == "pair" else None, 1.25, 0.5)
+    if mode == "pair":
+        assert_within_tol(to_bits(d[0]), ref[0], k, "bf16", what="bf16 D0")
+        assert_within_tol(to_bits(d[1]), ref[1], k, "bf16", what="bf16 D1")
+    else:
+        assert_within_tol(to_bits(d), ref, k, "bf16", sum_terms=2, what="bf16 sum")
+
+
+def test_rowreduce_bf16_and_batched_bf16():
+    m, n, k = 700, 264, 520
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=152, dtype="bf16")
+    D, y = cy.gemm_rowreduce(to_dev(A, "bf16"), to_dev(B, "bf16"))
+    assert_within_tol(to_bits(D), oracle.gemm("bf16", A, B), k, "bf16", what="bf16 rowreduce D")
+    yref = oracle.rowsum("bf16", A)
+    assert (np.abs(y.cpu().numpy() - yref) <= oracle.tolerance(yref, k)).all()
+    L = 6
+    Ab, Bb, _ = synth.gemm_inputs(136, 200, 264, seed=153, dtype="bf16", batch=L, kind="int")
+    Db = to_bits(cy.gemm_batched(to_dev(Ab, "bf16"), to_dev(Bb, "bf16")))
+    assert_bits_equal(Db, oracle.encode("bf16", oracle.gemm_batched("bf16", Ab, Bb)), "bf16 batched int")
+
+
+def test_long_k_accuracy():
+    """K = 32768: fp32 tensor-core accumulation stays inside the tolerance (reading R13)."""
+    m, n, k = 256, 512, 32768
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=154)
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    r = assert_within_tol(D, oracle.gemm("f16", A, B), k, "f16", what="K=32768")
+    assert r < 0.5  # at least 2x margin
+
+
+def test_large_integer_partials_exact():
+    """Integer inputs with partial sums up to 4*K = 32768 > fp16 range: fp32 accumulation is exact,
+    only the final RN-to-fp16 rounds (readings R3, R11)."""
+    m, n, k = 256, 256, 8192
+    A = synth.f64_to_bits(np.full((m, k), 2.0), "f16")
+    B = synth.f64_to_bits(np.where(np.random.default_rng(0).random((k, n)) < 0.5, 2.0, -2.0), "f16")
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    assert_bits_equal(D, oracle.encode("f16", oracle.gemm("f16", A, B)), "partials to 2^15")
