@@ -265,6 +265,7 @@ def oracle_baseline(case, budget_s=12.0):
     import oracle
 
     kind, arrs = case
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     nth = oracle.num_threads()
     if kind == "batched":
         A, B = arrs
@@ -328,12 +329,20 @@ def main():
 
     import torch
 
+    # BENCH_FORCE_DEVICE / BENCH_BACKEND: test-only overrides that run several ranks on one GPU
+    # (gloo) to exercise the multi-rank code path; production runs use one GPU per rank + NCCL.
+    if "BENCH_FORCE_DEVICE" in os.environ:
+        local = int(os.environ["BENCH_FORCE_DEVICE"])
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     import paper_2504_07004_b200 as cy
 
     W = make_workload(args.workload, rank, world, device)
@@ -351,7 +360,8 @@ def main():
             return x
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        on_dev = dist.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device=device if on_dev else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -461,6 +471,7 @@ def reference_arm(args, rank, world):
     import synth
 
     oracle.build()
+    oracle.set_threads(len(os.sched_getaffinity(0)))  # torchrun sets OMP_NUM_THREADS=1
     name = args.workload
     if name == "gemm" or name.startswith("sweep-"):
         n = 8192 if name == "gemm" else int(name.split("-")[1])

@@ -80,6 +80,7 @@ def _load():
     lib.cyo_rowsum.argtypes = [ci, i64, i64, vp, i64, vp, vp, i64]
     lib.cyo_rowsum.restype = ci
     lib.cyo_num_threads.restype = ci
+    lib.cyo_set_threads.argtypes = [ci]
     _lib = lib
     return lib
 
@@ -116,6 +117,11 @@ def _rows(rows, m):
 
 def num_threads() -> int:
     return int(_load().cyo_num_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads for the oracle (bench: all host cores, whatever OMP_NUM_THREADS says)."""
+    _load().cyo_set_threads(int(n))
 
 
 def decode(dtype, bits) -> np.ndarray:

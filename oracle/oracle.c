@@ -279,6 +279,8 @@ int cyo_rowsum(int dt, int64_t m, int64_t k, const uint16_t* A, int64_t lda, dou
 #ifdef _OPENMP
 #include <omp.h>
 int cyo_num_threads(void) { return omp_get_max_threads(); }
+void cyo_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
 #else
 int cyo_num_threads(void) { return 1; }
+void cyo_set_threads(int n) { (void)n; }
 #endif

@@ -53,8 +53,11 @@ def _gather_rows(local_padded, m, per, world, group):
                        device=local_padded.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(full, local_padded.contiguous(), group=group)
-    else:  # gloo (CPU tests of the host logic)
-        dist.all_gather(list(full.chunk(world)), local_padded.contiguous(), group=group)
+    else:  # gloo (CPU tests of the host logic; CUDA tensors are staged through host memory)
+        host = full.cpu() if full.is_cuda else full
+        dist.all_gather(list(host.chunk(world)), local_padded.contiguous().cpu(), group=group)
+        if host is not full:
+            full.copy_(host)
     return full[:m]
 
 
