@@ -95,6 +95,16 @@ const int g_pdl = [] {
   const char* e = std::getenv("CY_PDL");
   return e ? std::atoi(e) : 1;
 }();
+// CY_SLEEP_NS: epilogue wait backoff cap in ns (0 = spin); tuning knob
+const int g_sleep_ns = [] {
+  const char* e = std::getenv("CY_SLEEP_NS");
+  return e ? std::atoi(e) : 0;
+}();
+// CY_A_REUSE=0 disables the A-operand collector reuse across the two accumulators (tuning knob)
+const int g_a_reuse = [] {
+  const char* e = std::getenv("CY_A_REUSE");
+  return e ? std::atoi(e) : 1;
+}();
 std::atomic<int> g_last{-1};
 std::atomic<int64_t> g_launches{0};
 
@@ -313,6 +323,8 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.group_m = g_group_m > 0 ? g_group_m : 8;
   p.l2_policy = g_l2_policy;
   p.debug = g_debug;
+  p.sleep_ns = g_sleep_ns;
+  p.a_reuse = g_a_reuse;
   p.y = y;
 
   {

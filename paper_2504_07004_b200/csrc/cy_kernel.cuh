@@ -44,6 +44,8 @@ struct Params {
   int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
   int debug;             // timing experiments only (results invalid): 1 = no TMA refill, 2 = no epilogue
+  int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
+  int sleep_ns;          // >0: epilogue waits for the accumulator with nanosleep backoff (cap, ns)
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride
 };
@@ -327,6 +329,26 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           else mma_f16<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
         }
       };
+      // both B slots of one k-block, interleaved per k16 step so the second MMA reuses the A
+      // operand the first one loaded (collector::a fill / lastuse) instead of re-reading smem
+      auto issue_both = [&](uint32_t d, int st, int kb) {
+        const uint32_t sA = sStage0 + st * C::STAGE_BYTES;
+        const uint32_t sB = sA + C::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
+          const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
+          const uint64_t bd0 = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
+          const uint64_t bd1 = sdesc_sw128(sB + C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
+          const uint32_t acc = (kb | kk) != 0;
+          if constexpr (C::VAR == V_DUAL_SUM) {
+            mma_f16_col<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
+            mma_f16_col<C::CG, 2>(d, ad, bd1, C::IDESC, 1u);
+          } else {
+            mma_f16_col<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
+            mma_f16_col<C::CG, 2>(d + C::BN, ad, bd1, C::IDESC, acc);
+          }
+        }
+      };
       auto release = [&](int st) {
         mma_commit<C::CG>(bEmpty + 8 * st, 0x3);  // frees the stage in both CTAs
         if constexpr (C::REDUCE) mma_commit<C::CG>(bMDone + 8 * st, 0x3);  // reducers may read it
@@ -342,8 +364,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           for (int kb = 0; kb < p.k_blocks; ++kb) {
             mbar_wait(bFull + 8 * stage, phase);
             tc_fence_after();
-#pragma unroll
-            for (int sl = 0; sl < C::NUM_B; ++sl) issue(d, stage, sl, kb);
+            if constexpr (C::NUM_B == 2) {
+              if (p.a_reuse) issue_both(d, stage, kb);
+              else { issue(d, stage, 0, kb); issue(d, stage, 1, kb); }
+            } else {
+              issue(d, stage, 0, kb);
+            }
             release(stage);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
@@ -364,6 +390,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           for (int kb = 0; kb < p.k_blocks; ++kb) {
             mbar_wait(bFull + 8 * stage, phase);
             tc_fence_after();
+            if (acc1 && held == 0 && p.a_reuse) {  // steady state: both accumulators, A reused
+              issue_both(d, stage, kb);
+              release(stage);
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
             issue(d, stage, 0, kb);
             if (!acc1 && mbar_test_wait(bTEmpty + 8, bph ^ 1)) {
               acc1 = true;
@@ -410,7 +442,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       tile_coords(p, t, b, mb, nb);
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
-      mbar_wait(bTFull + 8 * buf, bph);
+      if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
+      else mbar_wait(bTFull + 8 * buf, bph);
       tc_fence_after();
       const int row0 = mb * C::BM + rank * C::BM_CTA + 32 * q;
       if (p.debug & 2) {  // timing experiment: drop the epilogue
