@@ -14,6 +14,7 @@ header cites the PAPER.md passage each function follows:
 * ``gemm_batched``  L independent GEMMs
 * ``dual_gemm``     SUM: alpha*(A.B0 + A.B1)+beta*C P:1529; PAIR: BASELINE configs[3]
 * ``rowsum``        y(i) = sum_k A(i,k)
+* ``dual_glu``      act(alpha*A.B0) * (alpha*A.B1)    GLU, P:1532 (R14)
 * ``encode``/``decode``  IEEE RN-even 16-bit codecs (R7)
 
 Inputs are numpy ``uint16`` arrays of raw fp16/bf16 bit patterns, row-major;
@@ -79,6 +80,10 @@ def _load():
     lib.cyo_dual_gemm.restype = ci
     lib.cyo_rowsum.argtypes = [ci, i64, i64, vp, i64, vp, vp, i64]
     lib.cyo_rowsum.restype = ci
+    lib.cyo_dual_glu.argtypes = [ci, ci, i64, i64, i64, dbl, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64]
+    lib.cyo_dual_glu.restype = ci
+    lib.cyo_act.argtypes = [ci, dbl]
+    lib.cyo_act.restype = dbl
     lib.cyo_num_threads.restype = ci
     lib.cyo_set_threads.argtypes = [ci]
     _lib = lib
@@ -200,6 +205,32 @@ def dual_gemm(dtype, mode, A, B0, B1, C0=None, C1=None, alpha=1.0, beta=0.0, row
     if rc:
         raise RuntimeError("cyo_dual_gemm failed")
     return (D0, D1) if mode_i == 0 else D0
+
+
+ACTS = {"silu": 0, "gelu_tanh": 1}
+
+
+def act(name, x) -> np.ndarray:
+    """The oracle's activation (fp64), elementwise."""
+    f = _load().cyo_act
+    a = ACTS[name]
+    return np.vectorize(lambda v: f(a, float(v)), otypes=[np.float64])(np.asarray(x, dtype=np.float64))
+
+
+def dual_glu(dtype, act_name, A, B0, B1, alpha=1.0, rows=None) -> np.ndarray:
+    """fp64 D_ref = act(alpha*A.B0) * (alpha*A.B1)  (GLU)."""
+    m, k = A.shape
+    n = B0.shape[1]
+    pa, lda = _mat(A, "A")
+    pb0, ldb0 = _mat(B0, "B0")
+    pb1, ldb1 = _mat(B1, "B1")
+    pr, nr, _keep = _rows(rows, m)
+    D = np.empty((nr, n), dtype=np.float64)
+    rc = _load().cyo_dual_glu(_dt(dtype), ACTS[act_name], m, n, k, float(alpha), pa, lda, pb0, ldb0, pb1, ldb1,
+                              D.ctypes.data, n, pr, nr)
+    if rc:
+        raise RuntimeError("cyo_dual_glu failed")
+    return D
 
 
 def rowsum(dtype, A, rows=None) -> np.ndarray:

@@ -37,6 +37,7 @@
  * accumulator; this is the textbook triple loop with the j loop innermost so
  * rows of B stream.  beta == 0 means C is not read (BLAS rule, R4).
  */
+#define _DEFAULT_SOURCE
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -255,6 +256,42 @@ int cyo_dual_gemm(int dt, int mode, int64_t m, int64_t n, int64_t k, double alph
   free(B0d);
   free(B1d);
   return err ? -1 : 0;
+}
+
+/*
+ * GLU dual GEMM (R14; "Dual-GEMM is a core computation in Gated Linear Units",
+ * P:1532-1533):  D = act(alpha * A.B0) (elementwise *) (alpha * A.B1)
+ *   act 0 = SiLU:      x / (1 + exp(-x))
+ *   act 1 = GELU-tanh: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+ * Both products are the plain fp64 triple loop of cyo_gemm; the activation and the product are
+ * applied to the fp64 results.
+ */
+static double act_eval(int act, double x) {
+  if (act == 0) return x / (1.0 + exp(-x));
+  const double c = sqrt(2.0 / M_PI);
+  return 0.5 * x * (1.0 + tanh(c * (x + 0.044715 * x * x * x)));
+}
+
+double cyo_act(int act, double x) { return act_eval(act, x); }
+
+int cyo_dual_glu(int dt, int act, int64_t m, int64_t n, int64_t k, double alpha,
+                 const uint16_t* A, int64_t lda, const uint16_t* B0, int64_t ldb0,
+                 const uint16_t* B1, int64_t ldb1, double* Dref, int64_t lddref,
+                 const int64_t* rows, int64_t nrows) {
+  if (act != 0 && act != 1) return -1;
+  if (!rows) nrows = m;
+  if (nrows == 0 || n == 0) return 0;
+  double* X0 = (double*)malloc(sizeof(double) * (size_t)nrows * (size_t)n);
+  double* X1 = (double*)malloc(sizeof(double) * (size_t)nrows * (size_t)n);
+  if (!X0 || !X1) { free(X0); free(X1); return -1; }
+  int rc = cyo_gemm(dt, m, n, k, alpha, A, lda, B0, ldb0, 0.0, NULL, n, X0, n, rows, nrows);
+  if (!rc) rc = cyo_gemm(dt, m, n, k, alpha, A, lda, B1, ldb1, 0.0, NULL, n, X1, n, rows, nrows);
+  if (!rc)
+    for (int64_t r = 0; r < nrows; ++r)
+      for (int64_t j = 0; j < n; ++j) Dref[r * lddref + j] = act_eval(act, X0[r * n + j]) * X1[r * n + j];
+  free(X0);
+  free(X1);
+  return rc;
 }
 
 /*

@@ -332,3 +332,40 @@ def test_golden_fixtures(orc):
             assert np.array_equal(D, np.array(g["D_bits"], dtype=np.uint16)), f
         elif g["op"] == "rowsum":
             assert np.array_equal(orc.rowsum(dt, A), np.array(g["y"], dtype=np.float64)), f
+
+
+# --------------------------------------------------------------------------- GLU (NEXT-3)
+
+def test_act_vs_torch_float64(orc):
+    x = np.concatenate([np.linspace(-30, 30, 2001), [0.0, 1e-8, -1e-8, 88.0, -88.0]])
+    t = torch.from_numpy(x)
+    assert np.allclose(orc.act("silu", x), torch.nn.functional.silu(t).numpy(), rtol=1e-15, atol=1e-300)
+    # the tanh form cancels (1 + tanh -> 0) for x << 0: compare with an absolute floor of 1e-15 |x|
+    g = torch.nn.functional.gelu(t, approximate="tanh").numpy()
+    assert (np.abs(orc.act("gelu_tanh", x) - g) <= 1e-14 * np.abs(g) + 1e-15 * np.abs(x)).all()
+
+
+def test_silu_identities(orc):
+    # silu(x) - silu(-x) = x  (x*s(x) + x*s(-x)... = x since s(x) + s(-x) = 1), silu(0) = 0,
+    # slope at 0 = 1/2, silu(x) -> x for large x, -> 0 for very negative x
+    x = np.linspace(-20, 20, 401)
+    assert np.allclose(orc.act("silu", x) - orc.act("silu", -x), x, rtol=0, atol=1e-13)
+    assert orc.act("silu", [0.0])[0] == 0.0
+    h = 1e-6
+    assert abs((orc.act("silu", [h])[0] - orc.act("silu", [-h])[0]) / (2 * h) - 0.5) < 1e-9
+    assert abs(orc.act("silu", [40.0])[0] - 40.0) < 1e-12 and abs(orc.act("silu", [-40.0])[0]) < 1e-15
+
+
+def test_dual_glu_vs_products(orc):
+    """GLU = act(alpha*A.B0) * (alpha*A.B1); integer inputs make both products exact, so the check
+    reduces to the (library-pinned) activation of exact integers."""
+    A, B0, B1, _, _ = synth.dual_inputs(37, 29, 120, seed=161, kind="int")
+    for name, fn in (("silu", torch.nn.functional.silu),
+                     ("gelu_tanh", lambda t: torch.nn.functional.gelu(t, approximate="tanh"))):
+        D = orc.dual_glu("f16", name, A, B0, B1, alpha=0.5)
+        x0 = 0.5 * (np_decode("f16", A).astype(np.int64) @ np_decode("f16", B0).astype(np.int64))
+        x1 = 0.5 * (np_decode("f16", A).astype(np.int64) @ np_decode("f16", B1).astype(np.int64))
+        ref = fn(torch.from_numpy(x0.astype(np.float64))).numpy() * x1
+        assert np.allclose(D, ref, rtol=1e-14, atol=1e-12)
+    rows = np.array([3, 0, 36])
+    assert np.array_equal(orc.dual_glu("f16", "silu", A, B0, B1, rows=rows), orc.dual_glu("f16", "silu", A, B0, B1)[rows])
