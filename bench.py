@@ -227,6 +227,29 @@ def make_workload(name, rank, world, device):
                  desc=f"batched fp16 GEMM 64 x 1024^3 (configs[2]), batch-sharded over {world} GPU(s)",
                  h2d=2 * hA.numel() * 2, d2h=hD.numel() * 2, shape={"batch": L_total, "m": m, "n": m, "k": m},
                  oracle_case=("batched", (A, B)), kernel_flops=2.0 * L * m ** 3)
+    elif name == "glu":
+        n = 8192
+        m_rank = n // world if world > 1 else n
+        A = synth.uniform((m_rank, n), synth.seed_for(3, 10 * rank))
+        B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
+        B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
+        dA, dB0, dB1 = up(A), up(B0), up(B1)
+        D0 = torch.empty((m_rank, n), dtype=torch.float16, device=device)
+
+        def step(i):
+            cy.dual_gemm_glu(dA, dB0, dB1, act="silu", out=D0)
+        hA, hB0, hB1 = pinned(A), pinned(B0), pinned(B1)
+        hD0 = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
+
+        def e2e_step(i):
+            cy.dual_gemm_glu(hA.to(device, non_blocking=True), hB0.to(device, non_blocking=True),
+                             hB1.to(device, non_blocking=True), act="silu", out=D0)
+            hD0.copy_(D0, non_blocking=True)
+        W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
+                 desc="GLU dual-GEMM D = silu(A*B0) * (A*B1), 8192^3 (SURVEY NEXT-3, P:1532)",
+                 h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=hD0.numel() * 2,
+                 shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("dual", (A, B0, B1)),
+                 kernel_flops=4.0 * m_rank * n * n)
     elif name == "dual":
         n = 8192
         m_rank = n // world if world > 1 else n
@@ -428,7 +451,7 @@ def main():
         cpu = oracle_baseline(W["oracle_case"])
 
     if rank == 0:
-        kcfg = cy.last_config()
+        kinfo = cy.last_kernel_info()
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
@@ -437,7 +460,7 @@ def main():
             "config": {"workload": W["desc"], **W["shape"],
                        "parallelism": f"M-row shards x{world}, B replicated, no collective" if args.workload != "allgather" else f"M-row shards x{world} + NCCL all-gather",
                        "l2": "inputs rotate over 2 sets (> 126 MB L2 total)" if W["flops"] > 1e12 or args.workload == "batched" else "inputs rotate over 2 sets",
-                       "kernel_config": cy.config_info(kcfg) if kcfg >= 0 else None},
+                       "kernel_config": kinfo},
             "pct_of_dense_peak": round(100.0 * value / world / peak, 2),
             "pct_of_nominal_2250": round(100.0 * value / world / 2250.0, 2),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
@@ -501,6 +524,29 @@ def reference_arm(args, rank, world):
             for r in np.unique(rows // 1024):
                 oracle.gemm("f16", A[r], B[r], rows=rows[rows // 1024 == r] % 1024)
         desc = "batched fp16 GEMM 64 x 1024^3"
+    elif name == "glu":
+        n = 8192
+        m_rank = n // world if world > 1 else n
+        A = synth.uniform((m_rank, n), synth.seed_for(3, 10 * rank))
+        B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
+        B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
+        dA, dB0, dB1 = up(A), up(B0), up(B1)
+        D0 = torch.empty((m_rank, n), dtype=torch.float16, device=device)
+
+        def step(i):
+            cy.dual_gemm_glu(dA, dB0, dB1, act="silu", out=D0)
+        hA, hB0, hB1 = pinned(A), pinned(B0), pinned(B1)
+        hD0 = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
+
+        def e2e_step(i):
+            cy.dual_gemm_glu(hA.to(device, non_blocking=True), hB0.to(device, non_blocking=True),
+                             hB1.to(device, non_blocking=True), act="silu", out=D0)
+            hD0.copy_(D0, non_blocking=True)
+        W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
+                 desc="GLU dual-GEMM D = silu(A*B0) * (A*B1), 8192^3 (SURVEY NEXT-3, P:1532)",
+                 h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=hD0.numel() * 2,
+                 shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("dual", (A, B0, B1)),
+                 kernel_flops=4.0 * m_rank * n * n)
     elif name == "dual":
         n = 8192
         A = synth.uniform((n, n), synth.seed_for(3, 0))

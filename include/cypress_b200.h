@@ -84,6 +84,18 @@ cy_status_t cy_dual_gemm(cy_dtype_t dt, cy_dual_mode_t mode, int64_t m, int64_t 
                          const void* C1, int64_t ldc1, void* D0, int64_t ldd0, void* D1,
                          int64_t ldd1, void* stream);
 
+/* GLU activation for cy_dual_gemm_glu. */
+typedef enum { CY_ACT_SILU = 0, CY_ACT_GELU_TANH = 1 } cy_act_t;
+
+/* Dual GEMM with a gated-linear-unit epilogue (the use the paper gives for dual-GEMM,
+ * P:1532-1533):  D = act(alpha*A*B0) (elementwise *) (alpha*A*B1),
+ * act = SiLU (x / (1 + e^-x)) or GELU in its tanh form; both products accumulate in fp32 TMEM and
+ * the activation and product are applied in fp32 before one RN cast (R14).  The two
+ * products are never written to memory.  D is m x n; D must not overlap A, B0 or B1. */
+cy_status_t cy_dual_gemm_glu(cy_dtype_t dt, cy_act_t act, int64_t m, int64_t n, int64_t k, float alpha,
+                             const void* A, int64_t lda, const void* B0, int64_t ldb0, const void* B1,
+                             int64_t ldb1, void* D, int64_t ldd, void* stream);
+
 /* GEMM + row reduction: "C = A.B and y(i) = sum_k A(i,k)" in a single kernel,
  * the reduction done on SIMT warps from the shared-memory A tiles while the
  * tensor core computes A.B.  y: m floats (fp32, device),
@@ -108,6 +120,11 @@ cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int
 cy_status_t cy_force_config(int id);
 /* Config id chosen by the most recent successful launch in this process (-1 if none). */
 int cy_last_config(void);
+/* Exact kernel of the most recent successful launch: variant (0 GEMM/batched, 1 dual pair, 2 dual
+ * sum, 3 row-reduce, 4 dual GLU), cta_group, tile_m, tile_n, stages, threads per CTA, dynamic smem
+ * bytes, dtype.  Any pointer may be NULL.  CY_ERR_INVALID_VALUE if nothing was launched yet. */
+cy_status_t cy_last_kernel_info(int* variant, int* cta_group, int* tile_m, int* tile_n, int* stages,
+                                int* threads, int* smem_bytes, int* dtype);
 /* Number of kernel launches this library issued in this process (monotone counter). */
 int64_t cy_launch_count(void);
 

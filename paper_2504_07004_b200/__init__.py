@@ -12,6 +12,7 @@ Entry points (same names as the C ABI, plus torch conveniences):
   gemm_batched(A, B, C=None, alpha=1, beta=0, out=None)    -> D (L,m,n)    cy_gemm_batched
   dual_gemm(A, B0, B1, C0=None, C1=None, mode="pair", ...) -> (D0, D1) | D cy_dual_gemm
   gemm_rowreduce(A, B, C=None, alpha=1, beta=0, ...)       -> (D, y)       cy_gemm_rowreduce
+  dual_gemm_glu(A, B0, B1, act="silu", alpha=1, out=None)  -> D            cy_dual_gemm_glu
 Raw pointer calls: ``paper_2504_07004_b200.cy_gemm(...)`` etc. (ctypes signatures of the header).
 """
 from __future__ import annotations
@@ -20,8 +21,8 @@ from . import _lib
 from ._lib import CY_BF16, CY_DUAL_PAIR, CY_DUAL_SUM, CY_F16, CyError, check
 
 __all__ = [
-    "gemm", "gemm_batched", "dual_gemm", "gemm_rowreduce", "CyError", "force_config", "last_config",
-    "num_configs", "config_info", "launch_count", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
+    "gemm", "gemm_batched", "dual_gemm", "dual_gemm_glu", "gemm_rowreduce", "CyError", "force_config", "last_config",
+    "num_configs", "config_info", "launch_count", "last_kernel_info", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
     "cy_gemm_rowreduce", "CY_F16", "CY_BF16", "CY_DUAL_PAIR", "CY_DUAL_SUM",
 ]
 
@@ -152,6 +153,21 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
     return (out0, out1) if pair else out0
 
 
+def dual_gemm_glu(A, B0, B1, act: str = "silu", alpha: float = 1.0, out=None, stream=None):
+    """D = act(alpha*A@B0) * (alpha*A@B1), act in {"silu", "gelu_tanh"} (GLU).  cy_dual_gemm_glu."""
+    _check_dev(A, B0, B1, out)
+    m, k = A.shape
+    n = B0.shape[1]
+    a = {"silu": _lib.CY_ACT_SILU, "gelu_tanh": _lib.CY_ACT_GELU_TANH}[act]
+    if out is None:
+        out = _empty2d(m, n, A)
+    st = _lib.load().cy_dual_gemm_glu(_dt(A), a, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
+                                      _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), _ptr(out), _ld(out, "out"),
+                                      _stream(stream, A))
+    check(st, "cy_dual_gemm_glu")
+    return out
+
+
 def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, y=None, stream=None):
     """D = alpha*A@B + beta*C and y[i] = sum_k A[i,k] (fp32), one kernel.  cy_gemm_rowreduce."""
     torch = _torch()
@@ -188,6 +204,22 @@ def config_info(cfg_id: int) -> dict:
     v = [ctypes.c_int() for _ in range(4)]
     check(_lib.load().cy_config_info(int(cfg_id), *[ctypes.byref(x) for x in v]), "cy_config_info")
     return {"cta_group": v[0].value, "tile_m": v[1].value, "tile_n": v[2].value, "stages": v[3].value}
+
+
+VARIANTS = {0: "gemm", 1: "dual_pair", 2: "dual_sum", 3: "rowreduce", 4: "dual_glu"}
+
+
+def last_kernel_info() -> dict:
+    """Exact kernel (variant, tile, stages, threads, smem) of the most recent launch."""
+    import ctypes
+
+    v = [ctypes.c_int() for _ in range(8)]
+    check(_lib.load().cy_last_kernel_info(*[ctypes.byref(x) for x in v]), "cy_last_kernel_info")
+    keys = ("variant", "cta_group", "tile_m", "tile_n", "stages", "threads", "smem_bytes", "dtype")
+    d = dict(zip(keys, (x.value for x in v)))
+    d["variant"] = VARIANTS.get(d["variant"], d["variant"])
+    d["dtype"] = "f16" if d["dtype"] == 0 else "bf16"
+    return d
 
 
 def launch_count() -> int:

@@ -14,8 +14,9 @@ LIB_PATH = os.path.join(_HERE, "libcypress_b200.so")
 
 # Every symbol include/cypress_b200.h declares (checked by tests/test_abi_cpu.py).
 EXPORTS = (
-    "cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_gemm_rowreduce", "cy_status_string",
+    "cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce", "cy_status_string",
     "cy_num_configs", "cy_config_info", "cy_force_config", "cy_last_config", "cy_launch_count",
+    "cy_last_kernel_info",
 )
 
 CY_OK = 0
@@ -23,6 +24,7 @@ STATUS_NAMES = {0: "CY_OK", 1: "CY_ERR_INVALID_VALUE", 2: "CY_ERR_MISALIGNED",
                 3: "CY_ERR_UNSUPPORTED_DEVICE", 4: "CY_ERR_LAUNCH", 5: "CY_ERR_INTERNAL"}
 CY_F16, CY_BF16 = 0, 1
 CY_DUAL_PAIR, CY_DUAL_SUM = 0, 1
+CY_ACT_SILU, CY_ACT_GELU_TANH = 0, 1
 
 
 class CyError(RuntimeError):
@@ -50,9 +52,10 @@ def load():
                                     vp, i64, i64, vp, i64, i64, vp]
     lib.cy_dual_gemm.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, vp, i64, f32, vp, i64,
                                  vp, i64, vp, i64, vp, i64, vp]
+    lib.cy_dual_gemm_glu.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, vp, i64, vp, i64, vp]
     lib.cy_gemm_rowreduce.argtypes = [ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, i64,
                                       vp, vp]
-    for f in ("cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_gemm_rowreduce"):
+    for f in ("cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce"):
         getattr(lib, f).restype = ci
     lib.cy_status_string.argtypes = [ci]
     lib.cy_status_string.restype = ctypes.c_char_p
@@ -64,6 +67,8 @@ def load():
     lib.cy_force_config.restype = ci
     lib.cy_last_config.restype = ci
     lib.cy_launch_count.restype = i64
+    lib.cy_last_kernel_info.argtypes = [ctypes.POINTER(ci)] * 8
+    lib.cy_last_kernel_info.restype = ci
     _lib = lib
     return lib
 

@@ -57,6 +57,9 @@ void add_all(std::vector<KDesc>& v) {
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_DUAL_SUM>());
   v.push_back(kdesc<DT, 2, 128, 6, cy::V_DUAL_SUM>());
   v.push_back(kdesc<DT, 1, 128, 4, cy::V_DUAL_SUM>());
+  v.push_back(kdesc<DT, 2, 128, 6, cy::V_DUAL_GLU>());
+  v.push_back(kdesc<DT, 2, 256, 4, cy::V_DUAL_GLU>());
+  v.push_back(kdesc<DT, 1, 128, 4, cy::V_DUAL_GLU>());
 }
 
 const std::vector<KDesc>& menu() {
@@ -259,11 +262,12 @@ int pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms) {
   double best_cost = 0;
   for (size_t i = 0; i < mn.size(); ++i) {
     if (mn[i].var != var || mn[i].dt != dt) continue;
-    const bool dual = (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM);
-    const int acc_cols = (var == cy::V_DUAL_PAIR ? 2 : 1) * (dual ? mn[i].bn : mn[i].bn);
+    const bool dual = (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM || var == cy::V_DUAL_GLU);
+    const int acc_cols = ((var == cy::V_DUAL_PAIR || var == cy::V_DUAL_GLU) ? 2 : 1) * mn[i].bn;
+    (void)dual;
     const int single = acc_cols * 2 > 512;
     double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, sms);
-    if (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM) c *= 1.0;
+
     if (best < 0 || c < best_cost) { best = static_cast<int>(i); best_cost = c; }
   }
   return best;
@@ -277,7 +281,7 @@ struct Operand {
 
 cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, float alpha, Operand A,
                    Operand B0, Operand B1, float beta, Operand C0, Operand C1, Operand D0, Operand D1, float* y,
-                   void* stream) {
+                   void* stream, int act = 0) {
   int dev;
   DevState* st;
   cy_status_t s = device_state(dev, st);
@@ -325,6 +329,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.debug = g_debug;
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
+  p.act = act;
   p.y = y;
 
   {
@@ -425,6 +430,22 @@ int cy_last_config(void) {
 
 int64_t cy_launch_count(void) { return g_launches.load(); }
 
+cy_status_t cy_last_kernel_info(int* variant, int* cta_group, int* tile_m, int* tile_n, int* stages, int* threads,
+                                int* smem_bytes, int* dtype) {
+  const int idx = g_last.load();
+  if (idx < 0) return CY_ERR_INVALID_VALUE;
+  const KDesc& k = menu()[idx];
+  if (variant) *variant = k.var;
+  if (cta_group) *cta_group = k.cg;
+  if (tile_m) *tile_m = 128 * k.cg;
+  if (tile_n) *tile_n = k.bn;
+  if (stages) *stages = k.stages;
+  if (threads) *threads = k.threads;
+  if (smem_bytes) *smem_bytes = k.smem;
+  if (dtype) *dtype = k.dt;
+  return CY_OK;
+}
+
 static cy_status_t check_common(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch) {
   if (dt != CY_F16 && dt != CY_BF16) return CY_ERR_INVALID_VALUE;
   if (m < 0 || n < 0 || k < 0 || batch < 0) return CY_ERR_INVALID_VALUE;
@@ -502,6 +523,26 @@ cy_status_t cy_dual_gemm(cy_dtype_t dt, cy_dual_mode_t mode, int64_t m, int64_t 
   return launch(pair ? cy::V_DUAL_PAIR : cy::V_DUAL_SUM, dt, m, n, k, 1, alpha, {A, lda, 0}, {B0, ldb0, 0},
                 {B1, ldb1, 0}, beta, {C0, ldc0, 0}, {pair ? C1 : nullptr, ldc1, 0}, {D0, ldd0, 0},
                 {pair ? D1 : nullptr, ldd1, 0}, nullptr, stream);
+}
+
+cy_status_t cy_dual_gemm_glu(cy_dtype_t dt, cy_act_t act, int64_t m, int64_t n, int64_t k, float alpha,
+                             const void* A, int64_t lda, const void* B0, int64_t ldb0, const void* B1, int64_t ldb1,
+                             void* D, int64_t ldd, void* stream) {
+  cy_status_t s = check_common(dt, m, n, k, 1);
+  if (s != CY_OK) return s;
+  if (act != CY_ACT_SILU && act != CY_ACT_GELU_TANH) return CY_ERR_INVALID_VALUE;
+  if (m == 0 || n == 0) return CY_OK;
+  if (!D || (k > 0 && (!A || !B0 || !B1))) return CY_ERR_INVALID_VALUE;
+  if (ldd < n || (k > 0 && (lda < k || ldb0 < n || ldb1 < n))) return CY_ERR_INVALID_VALUE;
+  if (!aligned16(D) || !ld_ok(ldd)) return CY_ERR_MISALIGNED;
+  if (k > 0 && (!aligned16(A) || !aligned16(B0) || !aligned16(B1) || !ld_ok(lda) || !ld_ok(ldb0) || !ld_ok(ldb1)))
+    return CY_ERR_MISALIGNED;
+  const Range rD = span(D, m, n, ldd, 1, 0, 2);
+  if (k > 0 && (overlap(rD, span(A, m, k, lda, 1, 0, 2)) || overlap(rD, span(B0, k, n, ldb0, 1, 0, 2)) ||
+                overlap(rD, span(B1, k, n, ldb1, 1, 0, 2))))
+    return CY_ERR_INVALID_VALUE;
+  return launch(cy::V_DUAL_GLU, dt, m, n, k, 1, alpha, {A, lda, 0}, {B0, ldb0, 0}, {B1, ldb1, 0}, 0.0f,
+                {nullptr, 0, 0}, {nullptr, 0, 0}, {D, ldd, 0}, {nullptr, 0, 0}, nullptr, stream, static_cast<int>(act));
 }
 
 cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha, const void* A,

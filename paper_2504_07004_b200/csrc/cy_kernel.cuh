@@ -6,6 +6,7 @@
 //   V_DUAL_PAIR  D0 = alpha*A.B0 + beta*C0, D1 = alpha*A.B1 + beta*C1   (GLU core)
 //   V_DUAL_SUM   D  = alpha*(A.B0 + A.B1) + beta*C
 //   V_ROWREDUCE  D  = alpha*A.B + beta*C and y(i) = sum_k A(i,k)
+//   V_DUAL_GLU   D  = act(alpha*A.B0) * (alpha*A.B1), act = SiLU | GELU-tanh   (GLU)
 //
 // Structure (the B200 re-derivation of the paper's warp-specialised, pipelined Hopper kernel,
 // Fig. 3b, and of the passes' end state):
@@ -32,7 +33,7 @@
 
 namespace cy {
 
-enum Variant : int { V_GEMM = 0, V_DUAL_PAIR = 1, V_DUAL_SUM = 2, V_ROWREDUCE = 3 };
+enum Variant : int { V_GEMM = 0, V_DUAL_PAIR = 1, V_DUAL_SUM = 2, V_ROWREDUCE = 3, V_DUAL_GLU = 4 };
 
 struct Params {
   int M, N, K, L;        // problem (L = batch count)
@@ -44,6 +45,7 @@ struct Params {
   int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
   int debug;             // timing experiments only (results invalid): 1 = no TMA refill, 2 = no epilogue
+  int act;               // V_DUAL_GLU: 0 = SiLU, 1 = GELU (tanh form)
   int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
   int sleep_ns;          // >0: epilogue waits for the accumulator with nanosleep backoff (cap, ns)
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
@@ -60,14 +62,16 @@ struct Cfg {
   static constexpr int STAGES = STAGES_;
   static constexpr int VAR = VAR_;
   static constexpr int NSUB = NSUB_;          // GEMM: N sub-tiles per tile sharing each A stage
-  static constexpr bool DUAL = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM);
+  static constexpr bool DUAL = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM || VAR == V_DUAL_GLU);
+  static constexpr bool GLU = (VAR == V_DUAL_GLU);
   static constexpr int BM_CTA = 128;          // accumulator rows per CTA = TMEM lanes
   static constexpr int BM = BM_CTA * CG;      // MMA M = output tile height
   static constexpr int TILE_N = DUAL ? BN : NSUB * BN;  // output tile width
   static constexpr int BK = 64;               // one 128-byte swizzle atom of K per stage
   static constexpr int UMMA_K = 16;
   static constexpr int NUM_B = DUAL ? 2 : NSUB;  // B slots per stage
-  static constexpr int NUM_ACC = (VAR == V_DUAL_PAIR) ? 2 : (VAR == V_DUAL_SUM ? 1 : NSUB);
+  static constexpr int NUM_ACC = (VAR == V_DUAL_PAIR || GLU) ? 2 : (VAR == V_DUAL_SUM ? 1 : NSUB);
+  static constexpr int NUM_OUT = GLU ? 1 : NUM_ACC;  // output tiles the epilogue writes per tile
   static constexpr int BN_CTA = BN / CG;      // B columns held per CTA
   static constexpr int A_BYTES = BM_CTA * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
@@ -95,7 +99,7 @@ struct Cfg {
   static constexpr bool REDUCE = (VAR == V_ROWREDUCE);
   // Single-buffered TMEM with two accumulators: the epilogue releases them one at a time and the
   // MMA issuer starts the next tile on accumulator 0 while accumulator 1 drains.
-  static constexpr bool SPLIT = (NUM_ACC_BUF == 1 && NUM_ACC == 2);
+  static constexpr bool SPLIT = (NUM_ACC_BUF == 1 && NUM_ACC == 2 && !GLU);
 
   static_assert(BN % 64 == 0 && BN_CTA % 64 == 0, "B is loaded in 64-column swizzle atoms");
   static_assert(BN >= 64 && BN <= 256, "tcgen05 kind::f16 N range");
@@ -120,6 +124,14 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& b, int&
   const int rg = r - g * group;
   mb = first_m + rg % gm;
   nb = rg / gm;
+}
+
+// GLU activations in fp32 (reading R14): SiLU x / (1 + e^-x); GELU tanh form
+// 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).
+__device__ __forceinline__ float act_f32(int act, float x) {
+  if (act == 0) return x / (1.0f + __expf(-x));
+  const float c = 0.7978845608028654f;
+  return 0.5f * x * (1.0f + tanhf(c * fmaf(0.044715f * x, x * x, x)));
 }
 
 template <int DT>
@@ -459,7 +471,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         continue;
       }
 #pragma unroll 1
-      for (int a = 0; a < C::NUM_ACC; ++a) {
+      for (int a = 0; a < C::NUM_OUT; ++a) {
         const bool second = (C::VAR == V_DUAL_PAIR && a == 1);
         const CUtensorMap* tmD = second ? &tmD1 : &tmD0;
         const CUtensorMap* tmC = second ? &tmC1 : &tmC0;
@@ -478,18 +490,27 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             cphase ^= 1;
           }
           uint32_t r0[32], r1[32];
+          uint32_t g0[C::GLU ? 32 : 1], g1[C::GLU ? 32 : 1];  // GLU: the gate operand (accumulator 1)
           if (p.k_blocks > 0) {
             const uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + buf * C::ACC_COLS + a * C::BN + 64 * c;
             tmem_ld_32x32b_x32(ta, r0);
             tmem_ld_32x32b_x32(ta + 32, r1);
+            if constexpr (C::GLU) {
+              tmem_ld_32x32b_x32(ta + C::BN, g0);
+              tmem_ld_32x32b_x32(ta + C::BN + 32, g1);
+            }
             tmem_ld_wait();
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) r0[i] = r1[i] = 0u;
+            if constexpr (C::GLU) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) g0[i] = g1[i] = 0u;
+            }
           }
           // The last chunk of this accumulator (buffer) is in registers: hand the TMEM columns back
           // to the MMA issuer before converting and storing it.
-          if (c + C::EPI_SPLIT >= C::BN / 64 && (C::SPLIT || a == C::NUM_ACC - 1)) {
+          if (c + C::EPI_SPLIT >= C::BN / 64 && (C::SPLIT || a == C::NUM_OUT - 1)) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -510,6 +531,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               const int col = 8 * v + e;
               const float x = __uint_as_float(col < 32 ? r0[col] : r1[col - 32]);
               f[e] = unit_alpha ? x : x * p.alpha;
+              if constexpr (C::GLU) {
+                const float gx = __uint_as_float(col < 32 ? g0[col] : g1[col - 32]);
+                const float u = unit_alpha ? gx : gx * p.alpha;
+                f[e] = act_f32(p.act, f[e]) * u;
+              }
             }
             if (p.has_c) {
               uint32_t cv[4];

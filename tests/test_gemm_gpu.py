@@ -358,3 +358,45 @@ def test_large_integer_partials_exact():
     B = synth.f64_to_bits(np.where(np.random.default_rng(0).random((k, n)) < 0.5, 2.0, -2.0), "f16")
     D = run_gemm(A, B, None, 1.0, 0.0, "f16")
     assert_bits_equal(D, oracle.encode("f16", oracle.gemm("f16", A, B)), "partials to 2^15")
+
+
+# ---------------------------------------------------------------- GLU dual epilogue (NEXT-3)
+def _glu_tol(dtype, A, B0, B1, alpha, act, k, rows=None):
+    """Derived bound (DESIGN.md R14): each product carries the GEMM error e = 1e-3 sqrt(K) |alpha|;
+    |act'| <= 1.13 for SiLU / GELU-tanh, so |dD| <= 1.2 e (|x1| + |act(x0)|) + e^2, plus the
+    output rounding 2^-8 |D| (the BASELINE relative term)."""
+    x0 = oracle.gemm(dtype, A, B0, alpha=alpha, rows=rows)
+    x1 = oracle.gemm(dtype, A, B1, alpha=alpha, rows=rows)
+    e = 1e-3 * np.sqrt(k) * abs(alpha)
+    ref = oracle.dual_glu(dtype, act, A, B0, B1, alpha=alpha, rows=rows)
+    return ref, 2.0 ** -8 * np.abs(ref) + 1.2 * e * (np.abs(x1) + np.abs(oracle.act(act, x0))) + e * e
+
+
+@pytest.mark.parametrize("cfg", [-1, 0, 1, 3])
+@pytest.mark.parametrize("act", ["silu", "gelu_tanh"])
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_dual_glu(cfg, act, dtype):
+    m, n, k = 333, 264, 190
+    A, B0, B1, _, _ = synth.dual_inputs(m, n, k, seed=171, dtype=dtype)
+    cy.force_config(cfg)
+    D = to_bits(cy.dual_gemm_glu(to_dev(A, dtype), to_dev(B0, dtype), to_dev(B1, dtype), act=act, alpha=0.75))
+    ref, tol = _glu_tol(dtype, A, B0, B1, 0.75, act, k)
+    err = np.abs(decode(D, dtype) - ref)
+    assert (err <= tol).all(), (err / tol).max()
+
+
+def test_dual_glu_integer_and_large():
+    """Integer inputs: both products exact in fp32, so D differs from RN(ref) only by the fp32
+    activation (<= 2 ulp of fp32) -- compare exactly where the fp16 rounding is not a near-tie;
+    and the BASELINE configs[3] size 8192^3 on sampled rows."""
+    A, B0, B1, _, _ = synth.dual_inputs(520, 392, 300, seed=172, kind="int")
+    D = decode(to_bits(cy.dual_gemm_glu(to_dev(A, "f16"), to_dev(B0, "f16"), to_dev(B1, "f16"))), "f16")
+    ref = oracle.dual_glu("f16", "silu", A, B0, B1)
+    rnd = decode(oracle.encode("f16", ref), "f16")
+    assert (np.abs(D - rnd) <= 2.0 ** -10 * np.abs(rnd)).all()
+    n = 8192
+    A, B0, B1, _, _ = synth.dual_inputs(n, n, n, seed=synth.seed_for(3, 0))
+    D = to_bits(cy.dual_gemm_glu(to_dev(A, "f16"), to_dev(B0, "f16"), to_dev(B1, "f16")))
+    rows = synth.sample_rows(n, n_random=8)[::3]
+    ref, tol = _glu_tol("f16", A, B0, B1, 1.0, "silu", n, rows=rows)
+    assert (np.abs(decode(D[rows], "f16") - ref) <= tol).all()
