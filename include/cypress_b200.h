@@ -84,6 +84,21 @@ cy_status_t cy_dual_gemm(cy_dtype_t dt, cy_dual_mode_t mode, int64_t m, int64_t 
                          const void* C1, int64_t ldc1, void* D0, int64_t ldd0, void* D1,
                          int64_t ldd1, void* stream);
 
+/* Replicated GEMM -- the compute step fused with its collective (BASELINE
+ * configs[4] "M-sharded ... + all-gather"): computes this rank's M-row shard
+ * D_shard = alpha*A*B + beta*C (A: m x k, C: m x n) and the epilogue stores every output tile
+ * directly into each of the `ndst` (1..8) destination matrices at rows [row_offset, row_offset + m).
+ * D_dst[j] is the base of a rows_total x n row-major matrix with leading dimension ldd, in device
+ * memory addressable by the current device -- typically the replicated D of every GPU of the job
+ * mapped into this process (CUDA IPC / symmetric memory over NVLink), so no separate all-gather
+ * runs.  Stores never leave the shard's row block of a destination.  Completion follows stream
+ * order on this device; the caller synchronizes with the peers before they read (e.g. a device
+ * barrier after the kernel).  Destinations must not overlap each other, A, B or C. */
+cy_status_t cy_gemm_replicated(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha,
+                               const void* A, int64_t lda, const void* B, int64_t ldb, float beta,
+                               const void* C, int64_t ldc, void* const* D_dst, int ndst, int64_t ldd,
+                               int64_t row_offset, int64_t rows_total, void* stream);
+
 /* GLU activation for cy_dual_gemm_glu. */
 typedef enum { CY_ACT_SILU = 0, CY_ACT_GELU_TANH = 1 } cy_act_t;
 

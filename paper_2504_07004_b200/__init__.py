@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import CY_BF16, CY_DUAL_PAIR, CY_DUAL_SUM, CY_F16, CyError, check
 
 __all__ = [
-    "gemm", "gemm_batched", "dual_gemm", "dual_gemm_glu", "gemm_rowreduce", "CyError", "force_config", "last_config",
+    "gemm", "gemm_batched", "dual_gemm", "dual_gemm_glu", "gemm_rowreduce", "gemm_replicated", "CyError", "force_config", "last_config",
     "num_configs", "config_info", "launch_count", "last_kernel_info", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
     "cy_gemm_rowreduce", "CY_F16", "CY_BF16", "CY_DUAL_PAIR", "CY_DUAL_SUM",
 ]
@@ -151,6 +151,26 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
         _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, A))
     check(st, "cy_dual_gemm")
     return (out0, out1) if pair else out0
+
+
+def gemm_replicated(A, B, dsts, row_offset: int, rows_total: int, C=None, alpha: float = 1.0, beta: float = 0.0,
+                    stream=None):
+    """Compute D_shard = alpha*A@B + beta*C and store it at rows [row_offset, row_offset + m) of every
+    destination in ``dsts`` (2-D tensors or raw device addresses of rows_total x n matrices, same ld).
+    cy_gemm_replicated (fused replication; the destinations are usually peers' buffers)."""
+    import ctypes
+
+    _check_dev(A, B, C)
+    m, k = A.shape
+    n = B.shape[1]
+    ptrs = [d if isinstance(d, int) else d.data_ptr() for d in dsts]
+    ldd = next((_ld(d, "dst") for d in dsts if not isinstance(d, int)), (n + 7) // 8 * 8)
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    st = _lib.load().cy_gemm_replicated(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"),
+                                        float(beta), _ptr(C) if beta != 0 else None,
+                                        _ld(C, "C") if (C is not None and beta != 0) else n, arr, len(ptrs), ldd,
+                                        int(row_offset), int(rows_total), _stream(stream, A))
+    check(st, "cy_gemm_replicated")
 
 
 def dual_gemm_glu(A, B0, B1, act: str = "silu", alpha: float = 1.0, out=None, stream=None):

@@ -281,7 +281,7 @@ struct Operand {
 
 cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, float alpha, Operand A,
                    Operand B0, Operand B1, float beta, Operand C0, Operand C1, Operand D0, Operand D1, float* y,
-                   void* stream, int act = 0) {
+                   void* stream, int act = 0, const Operand* extra_dst = nullptr, int n_extra = 0) {
   int dev;
   DevState* st;
   cy_status_t s = device_state(dev, st);
@@ -314,6 +314,9 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   }
   ok = ok && enc(&tD0, D0, m, n, 64, 32);
   if (D1.ptr) ok = ok && enc(&tD1, D1, m, n, 64, 32);
+  cy::DstMaps extra;
+  std::memset(&extra, 0, sizeof(extra));
+  for (int j = 0; j < n_extra; ++j) ok = ok && enc(&extra.m[j], extra_dst[j], m, n, 64, 32);
   if (!ok) return CY_ERR_LAUNCH;
   (void)bn_cta;
 
@@ -330,6 +333,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
   p.act = act;
+  p.n_extra = n_extra;
   p.y = y;
 
   {
@@ -367,7 +371,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   attrs[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
-  void* args[] = {&tA, &tB0, &tB1, &tC0, &tC1, &tD0, &tD1, &p};
+  void* args[] = {&tA, &tB0, &tB1, &tC0, &tC1, &tD0, &tD1, &p, &extra};
   cudaError_t e = cudaLaunchKernelExC(&cfg, kd.fn, args);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -523,6 +527,37 @@ cy_status_t cy_dual_gemm(cy_dtype_t dt, cy_dual_mode_t mode, int64_t m, int64_t 
   return launch(pair ? cy::V_DUAL_PAIR : cy::V_DUAL_SUM, dt, m, n, k, 1, alpha, {A, lda, 0}, {B0, ldb0, 0},
                 {B1, ldb1, 0}, beta, {C0, ldc0, 0}, {pair ? C1 : nullptr, ldc1, 0}, {D0, ldd0, 0},
                 {pair ? D1 : nullptr, ldd1, 0}, nullptr, stream);
+}
+
+cy_status_t cy_gemm_replicated(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha, const void* A,
+                               int64_t lda, const void* B, int64_t ldb, float beta, const void* C, int64_t ldc,
+                               void* const* D_dst, int ndst, int64_t ldd, int64_t row_offset, int64_t rows_total,
+                               void* stream) {
+  cy_status_t s = check_common(dt, m, n, k, 1);
+  if (s != CY_OK) return s;
+  if (!D_dst || ndst < 1 || ndst > 1 + cy::kMaxExtraDst) return CY_ERR_INVALID_VALUE;
+  if (row_offset < 0 || rows_total < 0 || row_offset + m > rows_total) return CY_ERR_INVALID_VALUE;
+  if (m == 0 || n == 0) return CY_OK;
+  const bool has_c = beta != 0.0f;
+  if ((k > 0 && (!A || !B)) || (has_c && !C)) return CY_ERR_INVALID_VALUE;
+  if (ldd < n || (k > 0 && (lda < k || ldb < n)) || (has_c && ldc < n)) return CY_ERR_INVALID_VALUE;
+  if (!ld_ok(ldd)) return CY_ERR_MISALIGNED;
+  if (k > 0 && (!aligned16(A) || !aligned16(B) || !ld_ok(lda) || !ld_ok(ldb))) return CY_ERR_MISALIGNED;
+  if (has_c && (!aligned16(C) || !ld_ok(ldc))) return CY_ERR_MISALIGNED;
+  Operand dst[1 + cy::kMaxExtraDst];
+  for (int j = 0; j < ndst; ++j) {
+    if (!D_dst[j] || !aligned16(D_dst[j])) return D_dst[j] ? CY_ERR_MISALIGNED : CY_ERR_INVALID_VALUE;
+    // this shard's row block of destination j (TMA clips every store at the block's edge)
+    dst[j] = {static_cast<const char*>(D_dst[j]) + row_offset * ldd * 2, ldd, 0};
+    const Range rD = span(dst[j].ptr, m, n, ldd, 1, 0, 2);
+    if (k > 0 && (overlap(rD, span(A, m, k, lda, 1, 0, 2)) || overlap(rD, span(B, k, n, ldb, 1, 0, 2))))
+      return CY_ERR_INVALID_VALUE;
+    if (has_c && overlap(rD, span(C, m, n, ldc, 1, 0, 2))) return CY_ERR_INVALID_VALUE;
+    for (int i = 0; i < j; ++i)
+      if (overlap(rD, span(dst[i].ptr, m, n, ldd, 1, 0, 2))) return CY_ERR_INVALID_VALUE;
+  }
+  return launch(cy::V_GEMM, dt, m, n, k, 1, alpha, {A, lda, 0}, {B, ldb, 0}, {nullptr, 0, 0}, beta, {C, ldc, 0},
+                {nullptr, 0, 0}, dst[0], {nullptr, 0, 0}, nullptr, stream, 0, dst + 1, ndst - 1);
 }
 
 cy_status_t cy_dual_gemm_glu(cy_dtype_t dt, cy_act_t act, int64_t m, int64_t n, int64_t k, float alpha,

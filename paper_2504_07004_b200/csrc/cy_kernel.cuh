@@ -46,10 +46,18 @@ struct Params {
   float* y;              // V_ROWREDUCE: y[M]
   int debug;             // timing experiments only (results invalid): 1 = no TMA refill, 2 = no epilogue
   int act;               // V_DUAL_GLU: 0 = SiLU, 1 = GELU (tanh form)
+  int n_extra;           // number of extra D destinations in DstMaps (0 = D only)
   int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
   int sleep_ns;          // >0: epilogue waits for the accumulator with nanosleep backoff (cap, ns)
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride
+};
+
+// Extra destinations of every D tile (fused replication): tensor maps over this
+// shard's row block of the replicated D on other GPUs (peer memory mapped into this process).
+constexpr int kMaxExtraDst = 7;
+struct DstMaps {
+  CUtensorMap m[kMaxExtraDst];
 };
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
@@ -160,7 +168,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     cy_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmC0,
                     const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmD0,
-                    const __grid_constant__ CUtensorMap tmD1, const Params p) {
+                    const __grid_constant__ CUtensorMap tmD1, const Params p,
+                    const __grid_constant__ DstMaps extra) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-B alignment
@@ -554,6 +563,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           __syncwarp();
           if (lane == 0 && !(p.debug & 4)) {  // (debug 4: timing experiment without the D stores)
             tma_store_3d(tmD, sb, n0, row0, b);
+            for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
             bulk_commit();
           }
           if constexpr (C::EPI_BUFS == 2) slot ^= 1;

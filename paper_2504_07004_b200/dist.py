@@ -7,6 +7,11 @@ the sm_100a kernels and B is replicated.  Only when the caller asks for a replic
 (``replicate=True``) is D (and y) all-gathered over NCCL (NVLink / NVSwitch); row-major D makes
 each rank's shard a contiguous row block, so the gather needs no packing.
 
+Fused replication: ``replicate="fused"`` skips the all-gather; the kernel's
+epilogue stores each output tile into every rank's replicated D through peer mappings
+(``cy_gemm_replicated``).  It needs CUDA peer access (NVLink) and NCCL-backed symmetric memory;
+the kernel side is tested on one GPU with local destinations.
+
 Shard geometry: ``rows_per = ceil(m / world)`` rounded up to ``align`` (256 = the CTA-pair tile
 height, BASELINE configs[4]); rank r owns rows [r*rows_per, min(m, (r+1)*rows_per)).  Uneven
 tails are gathered through a padded buffer and sliced.
@@ -61,16 +66,46 @@ def _gather_rows(local_padded, m, per, world, group):
     return full[:m]
 
 
+_SYMM_CACHE = {}
+
+
+def _symm_buffer(rows, n, dtype, device, group):
+    """One symmetric-memory (NVLink-mapped) D buffer per (shape, dtype, group), reused across calls."""
+    from torch.distributed import _symmetric_memory as symm
+
+    key = (rows, n, dtype, device, id(group))
+    if key not in _SYMM_CACHE:
+        buf = symm.empty((rows, n), dtype=dtype, device=device)
+        hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        _SYMM_CACHE[key] = (buf, hdl)
+    return _SYMM_CACHE[key]
+
+
 def sharded_gemm(A_local, B, C_local=None, alpha=1.0, beta=0.0, *, m_total=None, group=None,
                  replicate=False, align=256, gemm_fn=None):
     """Rank-local D = alpha*A_local@B + beta*C_local (A_local = this rank's row block).
 
-    replicate=False: returns the local D block (no communication).
-    replicate=True:  returns the full (m_total x n) D on every rank via one all-gather.
+    replicate=False:   returns the local D block (no communication).
+    replicate=True:    returns the full (m_total x n) D on every rank via one NCCL all-gather.
+    replicate="fused": the GEMM epilogue writes every tile straight into every rank's replicated D
+                       (symmetric memory over NVLink, cy_gemm_replicated) -- no separate collective;
+                       a device barrier then orders the peers.  Returns a view of a cached
+                       symmetric buffer (overwritten by the next call with the same shape).
     """
-    gemm_fn = gemm_fn or _default_gemm()
     world, rank = _world(group)
     rows, n = A_local.shape[0], B.shape[1]
+    if replicate == "fused" and world > 1:
+        from . import gemm_replicated
+
+        m = m_total if m_total is not None else rows * world
+        start, _, per = shard_rows(m, world, rank, align)
+        buf, hdl = _symm_buffer(per * world, n, A_local.dtype, A_local.device, group)
+        ptrs = [int(hdl.buffer_ptrs[r]) for r in range(world)]
+        gemm_replicated(A_local, B, ptrs, row_offset=start, rows_total=per * world, C=C_local, alpha=alpha,
+                        beta=beta)
+        hdl.barrier(channel=0)  # every rank's stores are visible before anyone reads
+        return buf[:m]
+    gemm_fn = gemm_fn or _default_gemm()
     if not replicate or world == 1:
         return gemm_fn(A_local, B, C_local, alpha, beta)
     m = m_total if m_total is not None else rows * world

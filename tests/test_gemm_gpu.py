@@ -400,3 +400,37 @@ def test_dual_glu_integer_and_large():
     rows = synth.sample_rows(n, n_random=8)[::3]
     ref, tol = _glu_tol("f16", A, B0, B1, 1.0, "silu", n, rows=rows)
     assert (np.abs(decode(D[rows], "f16") - ref) <= tol).all()
+
+
+# ---------------------------------------------------------------- fused replication (NEXT-2)
+@pytest.mark.parametrize("ndst", [1, 3, 8])
+@pytest.mark.parametrize("cfg", [-1, 0, 3])
+def test_gemm_replicated_multi_destination(ndst, cfg):
+    """The epilogue stores each tile into every destination's row block [row_offset, +m) and nothing
+    else: on one GPU the 'peers' are local buffers (the NVLink case only changes the addresses)."""
+    m, n, k, rows_total, off = 600, 392, 264, 1600, 512
+    A, B, C = synth.gemm_inputs(m, n, k, seed=181 + ndst, kind="int", with_c=True)
+    canary = 1234.0
+    dsts = [torch.full((rows_total, n), canary, dtype=torch.float16, device="cuda") for _ in range(ndst)]
+    cy.force_config(cfg)
+    cy.gemm_replicated(to_dev(A, "f16"), to_dev(B, "f16"), dsts, row_offset=off, rows_total=rows_total,
+                       C=to_dev(C, "f16"), alpha=1.0, beta=-1.0)
+    torch.cuda.synchronize()
+    want = oracle.encode("f16", oracle.gemm("f16", A, B, C, 1.0, -1.0))
+    cb = np.float16(canary).view(np.uint16)
+    for j, d in enumerate(dsts):
+        full = to_bits(d)
+        assert_bits_equal(full[off:off + m], want, f"dst {j}")
+        assert (full[:off] == cb).all() and (full[off + m:] == cb).all(), f"dst {j} wrote outside its shard"
+
+
+def test_gemm_replicated_rejects_bad_args():
+    A = torch.zeros((256, 64), dtype=torch.float16, device="cuda")
+    B = torch.zeros((64, 128), dtype=torch.float16, device="cuda")
+    d = torch.zeros((512, 128), dtype=torch.float16, device="cuda")
+    with pytest.raises(cy.CyError):
+        cy.gemm_replicated(A, B, [d], row_offset=300, rows_total=512)  # 300 + 256 > 512
+    with pytest.raises(cy.CyError):
+        cy.gemm_replicated(A, B, [d] * 9, row_offset=0, rows_total=512)  # > 8 destinations
+    with pytest.raises(cy.CyError):
+        cy.gemm_replicated(A, B, [d, d], row_offset=0, rows_total=512)  # overlapping destinations
