@@ -69,7 +69,8 @@ cy_status_t cy_gemm(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha,
                     const void* C, int64_t ldc, void* D, int64_t ldd, void* stream);
 
 /* Strided batched GEMM: "L independent GEMMs in a single pass".
- * X_b = X + b*strideX (elements), b < batch; one launch covers all b. */
+ * X_b = X + b*strideX (elements), b < batch; one launch covers all b.  With batch > 1 every
+ * stride must be positive (no broadcast operands) and strideD >= m*ldd (outputs do not overlap). */
 cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch,
                             float alpha, const void* A, int64_t lda, int64_t strideA,
                             const void* B, int64_t ldb, int64_t strideB, float beta,

@@ -77,9 +77,21 @@ def _stream(stream, like=None):
 
 
 def _check_dev(*ts):
+    dev = None
     for t in ts:
-        if t is not None and not t.is_cuda:
+        if t is None:
+            continue
+        if not t.is_cuda:
             raise ValueError("cypress_b200: all tensors must be CUDA tensors (no CPU fallback)")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"cypress_b200: tensors on different devices ({dev} vs {t.device})")
+    if dev is not None and dev.index is not None:
+        torch = _torch()
+        if torch.cuda.current_device() != dev.index:
+            # the C ABI works on the current device: follow the tensors (torch semantics)
+            torch.cuda.set_device(dev.index)
 
 
 def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):

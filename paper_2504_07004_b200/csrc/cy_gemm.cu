@@ -466,12 +466,15 @@ cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int6
   const bool has_c = beta != 0.0f;
   if (!D || (k > 0 && (!A || !B)) || (has_c && !C)) return CY_ERR_INVALID_VALUE;
   if (ldd < n || (k > 0 && (lda < k || ldb < n)) || (has_c && ldc < n)) return CY_ERR_INVALID_VALUE;
-  if (batch > 1 && (strideA < 0 || strideB < 0 || strideC < 0 || strideD < 0)) return CY_ERR_INVALID_VALUE;
+  // batch strides must be positive (TMA has no zero stride; a broadcast operand is not supported)
+  if (batch > 1 && (strideA <= 0 || strideB <= 0 || (has_c && strideC <= 0) || strideD <= 0))
+    return CY_ERR_INVALID_VALUE;
   if (batch > 1 && strideD < m * ldd) return CY_ERR_INVALID_VALUE;  // D batches must not overlap
   if (!aligned16(D) || !ld_ok(ldd)) return CY_ERR_MISALIGNED;
   if (k > 0 && (!aligned16(A) || !aligned16(B) || !ld_ok(lda) || !ld_ok(ldb))) return CY_ERR_MISALIGNED;
   if (has_c && (!aligned16(C) || !ld_ok(ldc))) return CY_ERR_MISALIGNED;
-  if (batch > 1 && ((strideA % 8) || (strideB % 8) || (strideC % 8) || (strideD % 8))) return CY_ERR_MISALIGNED;
+  if (batch > 1 && ((strideA % 8) || (strideB % 8) || (has_c && (strideC % 8)) || (strideD % 8)))
+    return CY_ERR_MISALIGNED;
   const Range rD = span(D, m, n, ldd, batch, strideD, 2);
   if (k > 0 && (overlap(rD, span(A, m, k, lda, batch, strideA, 2)) || overlap(rD, span(B, k, n, ldb, batch, strideB, 2))))
     return CY_ERR_INVALID_VALUE;

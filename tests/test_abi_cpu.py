@@ -103,6 +103,12 @@ def test_invalid_values(lib):
                                  None) == 1
 
 
+def test_batched_zero_stride_rejected(lib):
+    # broadcast (stride 0) operands are not supported: clear INVALID_VALUE, not a launch failure
+    assert lib.cy_gemm_batched(0, 8, 8, 8, 2, 1.0, P, 8, 0, P * 2, 8, 64, 0.0, None, 8, 64, P * 4, 8, 64,
+                               None) == 1
+
+
 def test_misaligned(lib):
     f = lib.cy_gemm
     assert f(0, 8, 8, 8, 1.0, P + 2, 8, P * 2, 8, 0.0, None, 8, P * 4, 8, None) == 2  # A not 16-B aligned
