@@ -434,3 +434,25 @@ def test_gemm_replicated_rejects_bad_args():
         cy.gemm_replicated(A, B, [d] * 9, row_offset=0, rows_total=512)  # > 8 destinations
     with pytest.raises(cy.CyError):
         cy.gemm_replicated(A, B, [d, d], row_offset=0, rows_total=512)  # overlapping destinations
+
+
+def test_host_pipeline_overlapped_steps():
+    """paper_2504_07004_b200.stream.HostGemmPipeline: several host-resident GEMMs with overlapped
+    copies give the same bits as one-at-a-time calls (integer inputs: exact)."""
+    from paper_2504_07004_b200.stream import HostGemmPipeline
+
+    m, n, k, steps = 520, 392, 264, 5
+    pipe = HostGemmPipeline(m, n, k, device="cuda")
+    ins, outs = [], []
+    for s in range(steps):
+        A, B, _ = synth.gemm_inputs(m, n, k, seed=191 + s, kind="int")
+        ins.append((A, B))
+        hA = torch.from_numpy(A.view(np.int16)).view(torch.float16).pin_memory()
+        hB = torch.from_numpy(B.view(np.int16)).view(torch.float16).pin_memory()
+        hD = torch.empty((m, n), dtype=torch.float16).pin_memory()
+        outs.append(hD)
+        pipe.submit(hA, hB, hD)
+    pipe.synchronize()
+    for (A, B), hD in zip(ins, outs):
+        assert_bits_equal(hD.view(torch.int16).numpy().view(np.uint16),
+                          oracle.encode("f16", oracle.gemm("f16", A, B)), "pipeline step")
