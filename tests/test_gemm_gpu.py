@@ -456,3 +456,51 @@ def test_host_pipeline_overlapped_steps():
     for (A, B), hD in zip(ins, outs):
         assert_bits_equal(hD.view(torch.int16).numpy().view(np.uint16),
                           oracle.encode("f16", oracle.gemm("f16", A, B)), "pipeline step")
+
+
+# ---------------------------------------------------------------- SURVEY section 4 coverage
+EDGE = [1, 7, 63, 64, 65, 127, 129, 255, 257, 1000, 1023]
+_rng = np.random.default_rng(20250407)
+EDGE_CASES = [tuple(int(x) for x in _rng.choice(EDGE, 3)) for _ in range(24)]
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("shape", EDGE_CASES)
+def test_boundary_product_set_integer(dtype, shape):
+    """Sampled product set of the boundary sizes in m, n, k (heuristic config): bit-exact."""
+    m, n, k = shape
+    A, B, C = synth.gemm_inputs(m, n, k, seed=201 + m + 3 * n + 7 * k, dtype=dtype, kind="int", with_c=True)
+    D = run_gemm(A, B, C, 1.0, 1.0, dtype)
+    assert_bits_equal(D, oracle.encode(dtype, oracle.gemm(dtype, A, B, C, 1.0, 1.0)), f"{dtype} {shape}")
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_gemm_256_twenty_seeds(seed):
+    """configs[0] (256^3) over 20 seeds (SPEC S:685 asks >= 20), uniform[-1,1]."""
+    A, B, _ = synth.gemm_inputs(256, 256, 256, seed=synth.seed_for(0, 100 + seed))
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    assert_within_tol(D, oracle.gemm("f16", A, B), 256, "f16", what=f"seed {seed}")
+
+
+@pytest.mark.parametrize("cfg", [0, 5])
+def test_m_shards_bit_identical_to_full(cfg):
+    """Multi-GPU invariant on one GPU: every 256-aligned M-row shard computed on its own equals the
+    same rows of the full GEMM bit for bit (same config) -- what rank r of an M-sharded run returns."""
+    m, n, k, world = 2048, 1024, 2048, 4
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=211)
+    full = run_gemm(A, B, None, 1.0, 0.0, "f16", cfg)
+    from paper_2504_07004_b200.dist import shard_rows
+
+    for r in range(world):
+        s, e, _ = shard_rows(m, world, r)
+        part = run_gemm(np.ascontiguousarray(A[s:e]), B, None, 1.0, 0.0, "f16", cfg)
+        assert_bits_equal(part, full[s:e], f"shard {r}")
+
+
+def test_batch_shards_bit_identical_to_full():
+    L, m = 8, 512
+    A, B, _ = synth.gemm_inputs(m, m, m, seed=212, batch=L)
+    full = to_bits(cy.gemm_batched(to_dev(A, "f16"), to_dev(B, "f16")))
+    for s in range(0, L, 2):
+        part = to_bits(cy.gemm_batched(to_dev(A[s:s + 2], "f16"), to_dev(B[s:s + 2], "f16")))
+        assert_bits_equal(part, full[s:s + 2], f"batches {s}:{s + 2}")
