@@ -352,6 +352,8 @@ def main():
     ap.add_argument("--impl", default="cypress_b200", choices=["cypress_b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the K timed steps in a CUDA graph and time its replay (no host launch gaps)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -397,7 +399,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def timed(fn, steps, warmup, sample_clocks=True, pipe=None):
+    def timed(fn, steps, warmup, sample_clocks=True, pipe=None, use_graph=False):
         for i in range(warmup):
             fn(i)
         if pipe is not None:
@@ -411,14 +413,30 @@ def main():
             pipe.join(stream)
         e1.record(stream)
         torch.cuda.synchronize()
-        per_step = e0.elapsed_time(e1) > 0.2 and pipe is None
+        per_step = e0.elapsed_time(e1) > 0.2 and pipe is None and not use_graph
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps if per_step else 1)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps if per_step else 1)]
         n0 = cy.launch_count()
+        graph = None
+        if use_graph and pipe is None:
+            graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(graph, stream=side):
+                    for i in range(steps):
+                        fn(warmup + 1 + i)
+            stream.wait_stream(side)
+            torch.cuda.synchronize()
         sampler = ClockSampler(local)
         with sampler:
             barrier()
-            if per_step:
+            if graph and pipe is None:
+                # CUDA graph of the K steps (captured above): replay = device-bound step rate
+                starts[0].record(stream)
+                graph.replay()
+                ends[0].record(stream)
+            elif per_step:
                 for i in range(steps):
                     starts[i].record(stream)
                     fn(warmup + 1 + i)
@@ -441,7 +459,7 @@ def main():
     attempts = 0
     while True:
         attempts += 1
-        total_ms, per, launches, sampler = timed(W["step"], args.steps, args.warmup)
+        total_ms, per, launches, sampler = timed(W["step"], args.steps, args.warmup, use_graph=args.graph)
         if not sampler.rejected() or attempts >= 2:
             break
     total_ms = maxred(total_ms)
@@ -492,7 +510,8 @@ def main():
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
-            "timing": "CUDA events on the launching stream; barrier+sync both sides; max over ranks",
+            "timing": "CUDA events on the launching stream; barrier+sync both sides; max over ranks"
+                      + ("; K steps captured in one CUDA graph, replay timed" if args.graph else ""),
         }
         print(json.dumps(out), flush=True)
     if world > 1:
