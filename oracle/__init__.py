@@ -15,6 +15,7 @@ header cites the PAPER.md passage each function follows:
 * ``dual_gemm``     SUM: alpha*(A.B0 + A.B1)+beta*C P:1529; PAIR: BASELINE configs[3]
 * ``rowsum``        y(i) = sum_k A(i,k)
 * ``dual_glu``      act(alpha*A.B0) * (alpha*A.B1)    GLU, P:1532 (R14)
+* ``attention``     softmax(scale Q K^T) V, lse       Sec. 5.3, P:1594-1611 (FA2/FA3 forward)
 * ``encode``/``decode``  IEEE RN-even 16-bit codecs (R7)
 
 Inputs are numpy ``uint16`` arrays of raw fp16/bf16 bit patterns, row-major;
@@ -84,6 +85,8 @@ def _load():
     lib.cyo_dual_glu.restype = ci
     lib.cyo_act.argtypes = [ci, dbl]
     lib.cyo_act.restype = dbl
+    lib.cyo_attention.argtypes = [ci, i64, i64, i64, i64, dbl, ci, vp, vp, vp, vp, vp]
+    lib.cyo_attention.restype = ci
     lib.cyo_num_threads.restype = ci
     lib.cyo_set_threads.argtypes = [ci]
     _lib = lib
@@ -231,6 +234,22 @@ def dual_glu(dtype, act_name, A, B0, B1, alpha=1.0, rows=None) -> np.ndarray:
     if rc:
         raise RuntimeError("cyo_dual_glu failed")
     return D
+
+
+def attention(dtype, Q, K, V, scale=None, causal=False):
+    """fp64 (O, lse) of softmax(scale * Q K^T) V per (batch*head); Q: (BH, sq, d), K/V: (BH, sk, d)."""
+    Q, K, V = (np.ascontiguousarray(x, dtype=np.uint16) for x in (Q, K, V))
+    bh, sq, d = Q.shape
+    sk = K.shape[1]
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    O = np.empty((bh, sq, d), dtype=np.float64)
+    lse = np.empty((bh, sq), dtype=np.float64)
+    rc = _load().cyo_attention(_dt(dtype), bh, sq, sk, d, float(scale), int(bool(causal)), Q.ctypes.data,
+                               K.ctypes.data, V.ctypes.data, O.ctypes.data, lse.ctypes.data)
+    if rc:
+        raise RuntimeError("cyo_attention failed")
+    return O, lse
 
 
 def rowsum(dtype, A, rows=None) -> np.ndarray:

@@ -312,6 +312,56 @@ int cyo_rowsum(int dt, int64_t m, int64_t k, const uint16_t* A, int64_t lda, dou
   return 0;
 }
 
+/*
+ * Forward attention (paper Sec. 5.3, P:1594-1611 -- Flash Attention 2/3 compute
+ * exactly this; HeadDim 128, FP16):
+ *   S = scale * Q.K^T,  P = softmax_rows(S) (keys j > i masked when causal),  O = P.V,
+ *   lse_i = log(sum_j exp(S_ij)).
+ * Layout: Q [BH, sq, d], K and V [BH, sk, d], O [BH, sq, d] contiguous (BH = batch * heads).
+ * Plain definition in fp64: per row, the max-shifted exponentials, their sum, the weighted sum of
+ * V rows.  Causal masking keeps key j <= query i (top-left aligned).
+ */
+int cyo_attention(int dt, int64_t bh, int64_t sq, int64_t sk, int64_t d, double scale, int causal,
+                  const uint16_t* Q, const uint16_t* K, const uint16_t* V, double* O, double* lse) {
+  if (bh < 0 || sq < 0 || sk < 0 || d <= 0) return -1;
+  int err = 0;
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t h = 0; h < bh; ++h)
+    for (int64_t i = 0; i < sq; ++i) {
+      double* s = (double*)malloc(sizeof(double) * (size_t)(sk > 0 ? sk : 1));
+      if (!s) {
+#pragma omp atomic write
+        err = 1;
+        continue;
+      }
+      const uint16_t* q = Q + (h * sq + i) * d;
+      const int64_t nk = causal ? (i + 1 < sk ? i + 1 : sk) : sk;
+      double mx = -INFINITY;
+      for (int64_t j = 0; j < nk; ++j) {
+        const uint16_t* kr = K + (h * sk + j) * d;
+        double acc = 0.0;
+        for (int64_t t = 0; t < d; ++t) acc += decode1(dt, q[t]) * decode1(dt, kr[t]);
+        s[j] = scale * acc;
+        if (s[j] > mx) mx = s[j];
+      }
+      double l = 0.0;
+      for (int64_t j = 0; j < nk; ++j) {
+        s[j] = exp(s[j] - mx);
+        l += s[j];
+      }
+      double* o = O + (h * sq + i) * d;
+      for (int64_t t = 0; t < d; ++t) o[t] = 0.0;
+      for (int64_t j = 0; j < nk; ++j) {
+        const uint16_t* vr = V + (h * sk + j) * d;
+        for (int64_t t = 0; t < d; ++t) o[t] += s[j] * decode1(dt, vr[t]);
+      }
+      for (int64_t t = 0; t < d; ++t) o[t] = nk > 0 ? o[t] / l : 0.0;
+      if (lse) lse[h * sq + i] = nk > 0 ? mx + log(l) : -INFINITY;
+      free(s);
+    }
+  return err ? -1 : 0;
+}
+
 /* Threads the OpenMP runtime will use (for the cpu_baseline "cores" field). */
 #ifdef _OPENMP
 #include <omp.h>

@@ -369,3 +369,47 @@ def test_dual_glu_vs_products(orc):
         assert np.allclose(D, ref, rtol=1e-14, atol=1e-12)
     rows = np.array([3, 0, 36])
     assert np.array_equal(orc.dual_glu("f16", "silu", A, B0, B1, rows=rows), orc.dual_glu("f16", "silu", A, B0, B1)[rows])
+
+
+# --------------------------------------------------------------------------- attention (NEXT-4)
+
+def _t64(dtype, bits):
+    return torch.from_numpy(np_decode(dtype, bits))
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_vs_torch_sdpa_float64(orc, causal):
+    """Library special case: torch scaled_dot_product_attention in float64 on the decoded inputs."""
+    bh, sq, sk, d = 3, 37, 37 if causal else 53, 64
+    Q = synth.uniform((bh, sq, d), 231)
+    K = synth.uniform((bh, sk, d), 232)
+    V = synth.uniform((bh, sk, d), 233)
+    O, lse = orc.attention("f16", Q, K, V, causal=causal)
+    ref = torch.nn.functional.scaled_dot_product_attention(_t64("f16", Q), _t64("f16", K), _t64("f16", V),
+                                                           is_causal=causal).numpy()
+    assert np.allclose(O, ref, rtol=1e-12, atol=1e-13)
+    s = torch.einsum("hid,hjd->hij", _t64("f16", Q), _t64("f16", K)) / np.sqrt(d)
+    if causal:
+        s = s.masked_fill(torch.ones(sq, sk, dtype=torch.bool).triu(1), float("-inf"))
+    assert np.allclose(lse, torch.logsumexp(s, dim=-1).numpy(), rtol=1e-13, atol=1e-13)
+
+
+def test_attention_closed_forms(orc):
+    d = 128
+    V = synth.uniform((2, 40, d), 234)
+    K = synth.uniform((2, 40, d), 235)
+    # Q = 0: every score is 0, P is uniform -> O = mean of the V rows, lse = log(sk)
+    Q0 = synth.f64_to_bits(np.zeros((2, 5, d)), "f16")
+    O, lse = orc.attention("f16", Q0, K, V)
+    assert np.allclose(O, np_decode("f16", V).mean(axis=1, keepdims=True).repeat(5, axis=1), rtol=0, atol=1e-15)
+    assert np.allclose(lse, np.log(40.0), rtol=0, atol=1e-15)
+    # one key: O = that V row exactly; causal row 0 sees only key 0
+    O1, _ = orc.attention("f16", Q0[:, :1], K[:, :1], V[:, :1])
+    assert np.array_equal(O1[:, 0], np_decode("f16", V[:, 0]))
+    Qr = synth.uniform((2, 40, d), 236)
+    Oc, _ = orc.attention("f16", Qr, K, V, causal=True)
+    assert np.array_equal(Oc[:, 0], np_decode("f16", V[:, 0]))
+    # constant V rows: O = the constant for any scores
+    Vc = synth.f64_to_bits(np.full((2, 40, d), 0.375), "f16")
+    Oq, _ = orc.attention("f16", Qr, K, Vc)
+    assert np.allclose(Oq, 0.375, rtol=1e-15, atol=0)
