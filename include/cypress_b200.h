@@ -121,6 +121,18 @@ cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, fl
                               const void* C, int64_t ldc, void* D, int64_t ldd, float* y,
                               void* stream);
 
+/* Forward attention (the Flash Attention 2/3 forward of the paper's Sec. 5.3,
+ * P:1594-1664, FP16/BF16, HeadDim 128 -- P:1636):
+ *   O = softmax(scale * Q K^T) V  per (batch, head), rows masked to key <= query when causal
+ *   (top-left aligned);  lse[b*heads+h][i] = log sum_j exp(scale * q_i.k_j)  (natural log, fp32).
+ * Layout: Q [batch, heads, seq_q, 128], K and V [batch, heads, seq_k, 128], O like Q, all
+ * contiguous (row stride 128 elements).  Scores and O accumulate in fp32 (TMEM); the softmax runs
+ * in fp32 in the exp2 domain; P is rounded to the input type for the P.V product (as FA2/FA3 do).
+ * lse may be NULL.  head_dim must be 128; batch*heads <= 65535.  O must not overlap Q, K, V. */
+cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t heads, int64_t seq_q, int64_t seq_k,
+                             int64_t head_dim, float scale, int causal, const void* Q, const void* K,
+                             const void* V, void* O, float* lse, void* stream);
+
 /* Human-readable status. */
 const char* cy_status_string(cy_status_t s);
 

@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import CY_BF16, CY_DUAL_PAIR, CY_DUAL_SUM, CY_F16, CyError, check
 
 __all__ = [
-    "gemm", "gemm_batched", "dual_gemm", "dual_gemm_glu", "gemm_rowreduce", "gemm_replicated", "CyError", "force_config", "last_config",
+    "gemm", "gemm_batched", "dual_gemm", "dual_gemm_glu", "gemm_rowreduce", "gemm_replicated", "attention", "CyError", "force_config", "last_config",
     "num_configs", "config_info", "launch_count", "last_kernel_info", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
     "cy_gemm_rowreduce", "CY_F16", "CY_BF16", "CY_DUAL_PAIR", "CY_DUAL_SUM",
 ]
@@ -163,6 +163,29 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
         _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, A))
     check(st, "cy_dual_gemm")
     return (out0, out1) if pair else out0
+
+
+def attention(Q, K, V, scale=None, causal: bool = False, out=None, lse=None, stream=None):
+    """Forward attention O = softmax(scale Q K^T) V (FA2/FA3 forward, HeadDim 128).
+    Q: (batch, heads, seq_q, 128), K/V: (batch, heads, seq_k, 128), contiguous fp16/bf16.
+    Returns (O, lse) with lse (batch, heads, seq_q) fp32 natural log-sum-exp.  cy_attention_fwd."""
+    torch = _torch()
+    _check_dev(Q, K, V, out, lse)
+    b, h, sq, d = Q.shape
+    sk = K.shape[2]
+    for t, name in ((Q, "Q"), (K, "K"), (V, "V")):
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous (batch, heads, seq, head_dim)")
+    if scale is None:
+        scale = d ** -0.5
+    if out is None:
+        out = torch.empty_like(Q)
+    if lse is None:
+        lse = torch.empty((b, h, sq), dtype=torch.float32, device=Q.device)
+    st = _lib.load().cy_attention_fwd(_dt(Q), b, h, sq, sk, d, float(scale), int(bool(causal)), _ptr(Q), _ptr(K),
+                                      _ptr(V), _ptr(out), _ptr(lse), _stream(stream, Q))
+    check(st, "cy_attention_fwd")
+    return out, lse
 
 
 def gemm_replicated(A, B, dsts, row_offset: int, rows_total: int, C=None, alpha: float = 1.0, beta: float = 0.0,

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libcypress_b200.so")
 EXPORTS = (
     "cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce", "cy_status_string",
     "cy_num_configs", "cy_config_info", "cy_force_config", "cy_last_config", "cy_launch_count",
-    "cy_last_kernel_info", "cy_gemm_replicated",
+    "cy_last_kernel_info", "cy_gemm_replicated", "cy_attention_fwd",
 )
 
 CY_OK = 0
@@ -55,6 +55,8 @@ def load():
     lib.cy_dual_gemm_glu.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, vp, i64, vp, i64, vp]
     lib.cy_gemm_replicated.argtypes = [ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64,
                                        ctypes.POINTER(ctypes.c_void_p), ci, i64, i64, i64, vp]
+    lib.cy_attention_fwd.argtypes = [ci, i64, i64, i64, i64, i64, f32, ci, vp, vp, vp, vp, vp, vp]
+    lib.cy_attention_fwd.restype = ci
     lib.cy_gemm_rowreduce.argtypes = [ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, i64,
                                       vp, vp]
     for f in ("cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce",

@@ -26,7 +26,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = force or not os.path.exists(OUT) or any(os.path.getmtime(s) > os.path.getmtime(OUT) for s in sources())
     if stale:
         tmp = OUT + f".tmp{os.getpid()}"
-        cmd = [NVCC, *FLAGS, os.path.join(CSRC, "cy_gemm.cu"), "-o", tmp]
+        cmd = [NVCC, *FLAGS, os.path.join(CSRC, "cy_gemm.cu"), os.path.join(CSRC, "cy_attention.cu"), "-o", tmp]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -539,3 +539,81 @@ def test_cuda_graph_capture_and_replay():
         assert_bits_equal(to_bits(D1), want, "graph replay D1")
         assert_bits_equal(to_bits(D2), want, "graph replay D2")
     del dA2, dB2
+
+
+# ---------------------------------------------------------------- forward attention (NEXT-4)
+def _attn_inputs(b, h, sq, sk, seed, dtype="f16", qscale=1.0):
+    Q = synth.uniform((b * h, sq, 128), seed, dtype, lo=-qscale, hi=qscale)
+    K = synth.uniform((b * h, sk, 128), seed + 1, dtype)
+    V = synth.uniform((b * h, sk, 128), seed + 2, dtype)
+    return Q, K, V
+
+
+def _attn_check(dtype, b, h, Q, K, V, causal):
+    """Bound (R15): P is rounded to the input type before P.V (as FA2/FA3 do), so
+    |O - O_ref| <= u max|V| (rounded weights) + u |O_ref| (normaliser) + output rounding,
+    u = 2^-11 (fp16) / 2^-8 (bf16); the fp32 score / exp2 errors are ~1e-6 relative."""
+    bh, sq, _ = Q.shape
+    sk = K.shape[1]
+    dQ = to_dev(Q, dtype).view(b, h, sq, 128)
+    dK = to_dev(K, dtype).view(b, h, sk, 128)
+    dV = to_dev(V, dtype).view(b, h, sk, 128)
+    O, lse = cy.attention(dQ, dK, dV, causal=causal)
+    torch.cuda.synchronize()
+    Oref, lref = oracle.attention(dtype, Q, K, V, causal=causal)
+    u = 2.0 ** -11 if dtype == "f16" else 2.0 ** -8
+    vmax = np.abs(decode(V, dtype)).max() if sk else 0.0
+    tol = 2 * u * vmax + 3 * u * np.abs(Oref) + 1e-6
+    err = np.abs(decode(to_bits(O).reshape(bh, sq, 128), dtype) - Oref)
+    assert (err <= tol).all(), f"O: max err/tol {(err / tol).max():.3f}"
+    l = lse.reshape(bh, sq).cpu().numpy()
+    assert np.allclose(l, lref, rtol=0, atol=2e-3 + 4 * u), np.abs(l - lref).max()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", [(2, 3, 300, 500), (1, 2, 128, 128), (1, 1, 1, 1), (1, 2, 129, 257), (2, 2, 1024, 1024)])
+def test_attention_f16(shape, causal):
+    b, h, sq, sk = shape
+    if causal and sq > sk:
+        sk = sq
+    Q, K, V = _attn_inputs(b, h, sq, sk, seed=241 + sq + sk)
+    _attn_check("f16", b, h, Q, K, V, causal)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_peaky_and_bf16(causal):
+    """Sharp softmax (Q x 8: the running max moves a lot -> exercises the O rescale in TMEM)."""
+    Q, K, V = _attn_inputs(2, 2, 640, 640, seed=251, qscale=8.0)
+    _attn_check("f16", 2, 2, Q, K, V, causal)
+    Qb, Kb, Vb = _attn_inputs(1, 3, 384, 700, seed=252, dtype="bf16")
+    _attn_check("bf16", 1, 3, Qb, Kb, Vb, causal=False)
+
+
+def test_attention_closed_forms():
+    d = 128
+    _, K, V = _attn_inputs(1, 2, 1, 300, seed=253)
+    Q0 = np.zeros((2, 200, d), np.uint16)  # +0.0: every score 0 -> P = 1 exactly -> O = mean(V)
+    O, lse = cy.attention(to_dev(Q0, "f16").view(1, 2, 200, d), to_dev(K, "f16").view(1, 2, 300, d),
+                          to_dev(V, "f16").view(1, 2, 300, d))
+    mean = decode(V, "f16").mean(axis=1, keepdims=True)
+    got = decode(to_bits(O).reshape(2, 200, d), "f16")
+    assert np.allclose(got, mean, rtol=2.0 ** -10, atol=1e-5)
+    assert np.allclose(lse.cpu().numpy(), np.log(300.0), atol=1e-5)
+    # one key: O = V row 0 (bit-exact: p = 1, O = 1 * v / 1)
+    O1, _ = cy.attention(to_dev(Q0[:, :7], "f16").view(1, 2, 7, d), to_dev(K[:, :1], "f16").view(1, 2, 1, d),
+                         to_dev(V[:, :1], "f16").view(1, 2, 1, d))
+    assert_bits_equal(to_bits(O1).reshape(2, 7, d), np.repeat(V[:, :1], 7, axis=1), "one key")
+
+
+def test_attention_large_sampled():
+    """FA benchmark shape (16 heads x 4096, HeadDim 128), non-causal, oracle on sampled query rows."""
+    b, h, s = 1, 16, 4096
+    Q, K, V = _attn_inputs(b, h, s, s, seed=254)
+    dQ, dK, dV = (to_dev(x, "f16").view(b, h, s, 128) for x in (Q, K, V))
+    O, lse = cy.attention(dQ, dK, dV)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(s, n_random=8)[::5]
+    Oref, lref = oracle.attention("f16", np.ascontiguousarray(Q[:, rows]), K, V)
+    got = decode(to_bits(O).reshape(b * h, s, 128)[:, rows], "f16")
+    tol = 2 * 2.0 ** -11 * np.abs(decode(V, "f16")).max() + 3 * 2.0 ** -11 * np.abs(Oref) + 1e-6
+    assert (np.abs(got - Oref) <= tol).all()
