@@ -215,21 +215,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t tS = tmem + lane_base + TM_S0 + s * 128;
       const int key0 = j * BKV;
       const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= q0);
-      // pass 1: row max of this block (exp2 domain)
-      float mb = -INFINITY;
+      // key validity only matters in the last (ragged) block and in the causal diagonal block
+      auto valid = [&](int key) { return full_block || (key < p.sk && (!p.causal || key <= qrow)); };
+      // pass 1: row max of this block (exp2 domain); 8 independent partial maxima for ILP
+      float mx8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mx8[t] = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tS + 32 * c, v);
         tmem_ld_wait();
+        if (full_block) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int key = key0 + 32 * c + e;
-          const bool ok = full_block || (key < p.sk && (!p.causal || key <= qrow));
-          const float x = ok ? __uint_as_float(v[e]) * p.scale_log2 : -INFINITY;
-          mb = fmaxf(mb, x);
+          for (int e = 0; e < 32; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (valid(key0 + 32 * c + e)) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
         }
       }
+      float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;  // scale_log2 > 0 keeps the order
       const float m_new = fmaxf(m, mb);
       const float corr = (m_new == -INFINITY) ? 1.f : ex2(m - m_new);  // ex2(-inf) = 0
       const float msub = (m_new == -INFINITY) ? 0.f : m_new;
@@ -251,26 +259,26 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_st_wait();
         }
       }
-      // pass 2: P = exp2(x - m_new) -> shared (K-major SW128: atom = key / 64, 16-B chunk swizzled by row)
-      float sum = 0.f;
+      // pass 2: P = exp2(s * scale_log2 - m_new) -> shared (K-major SW128: atom = key / 64,
+      // 16-B chunk swizzled by row); 8 independent partial sums
+      float sm8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) sm8[t] = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tS + 32 * c, v);
         tmem_ld_wait();
+        float pe[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          pe[e] = ex2(fmaf(__uint_as_float(v[e]), p.scale_log2, -msub));
+          if (!full_block && !valid(key0 + 32 * c + e)) pe[e] = 0.f;
+          sm8[e & 7] += pe[e];
+        }
         uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float pe[2];
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const int key = key0 + 32 * c + e + t;
-            const bool ok = full_block || (key < p.sk && (!p.causal || key <= qrow));
-            pe[t] = ok ? ex2(__uint_as_float(v[e + t]) * p.scale_log2 - msub) : 0.f;
-            sum += pe[t];
-          }
-          pk[e / 2] = pack2<DT>(pe[0], pe[1]);
-        }
+        for (int e = 0; e < 16; ++e) pk[e] = pack2<DT>(pe[2 * e], pe[2 * e + 1]);
         const uint32_t atom = sP + (c >> 1) * ATOM + r * 128;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -278,6 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           st_shared_v4(atom + ((chunk ^ (r & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
+      const float sum = ((sm8[0] + sm8[1]) + (sm8[2] + sm8[3])) + ((sm8[4] + sm8[5]) + (sm8[6] + sm8[7]));
       l = l * corr + sum;
       m = m_new;
       tc_fence_before();
