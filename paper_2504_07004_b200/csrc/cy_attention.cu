@@ -74,6 +74,15 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem desc]: kind::f16, cta_group::1, A (K-major) read from tensor memory
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -184,19 +193,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (j + 1 < nkv) {  // next scores while the softmax of block j runs
           const int s1 = (j + 1) & 1;
           mbar_wait(bKVFull + 8 * s1, ((j + 1) >> 1) & 1);
-          if (j + 1 >= 2) mbar_wait(bSEmpty + 8 * s1, (((j + 1) >> 1) & 1) ^ 1);
+          // S buffer s1 held P_{j-1}; PV_{j-1} was issued before this MMA and tcgen05 ops execute
+          // in issue order, so the overwrite is safe without a barrier.
           tc_fence_after();
           issue_s(j + 1);
         }
         mbar_wait(bPReady, j & 1);
         tc_fence_after();
         const uint32_t v = sV + s * TILE;
+        // O += P_j V_j with P_j read from TMEM (packed 16-bit pairs over the S_j buffer, 8 columns
+        // per k16 step) and V_j from shared memory (MN-major)
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * ATOM + (kk & 3) * 32;
-          mma_f16<1>(tmem + TM_O, sdesc_sw128(sP + aoff, 16, 1024), sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV,
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_f16_ts(tmem + TM_O, tmem + TM_S0 + s * 128 + kk * 8, sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV,
                      (j | kk) != 0);
-        }
         mma_commit<1>(bOReady, 0);
         mma_commit<1>(bKVEmpty + 8 * s, 0);
       }
@@ -217,85 +227,70 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= q0);
       // key validity only matters in the last (ragged) block and in the causal diagonal block
       auto valid = [&](int key) { return full_block || (key < p.sk && (!p.causal || key <= qrow)); };
-      // pass 1: row max of this block (exp2 domain); 8 independent partial maxima for ILP
+      // S_j row -> registers (one TMEM read), masked keys -> -inf
+      uint32_t v[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * c]));
+      tmem_ld_wait();
+      if (!full_block) {
+#pragma unroll
+        for (int e = 0; e < 128; ++e)
+          if (!valid(key0 + e)) v[e] = __float_as_uint(-INFINITY);
+      }
       float mx8[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) mx8[t] = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + 32 * c, v);
-        tmem_ld_wait();
-        if (full_block) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (valid(key0 + 32 * c + e)) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
-        }
-      }
+      for (int e = 0; e < 128; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
       float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;  // scale_log2 > 0 keeps the order
-      const float m_new = fmaxf(m, mb);
-      const float corr = (m_new == -INFINITY) ? 1.f : ex2(m - m_new);  // ex2(-inf) = 0
+      // Lazy rescaling: keep the running max unless it grows by more than 2^8 (P <= 256 stays exact
+      // in the 16-bit types and the fp32 sums); the final O / l uses the same max, so this is exact.
+      float m_new = m, corr = 1.f;
+      if (mb > m + 8.f) {
+        m_new = mb;
+        corr = ex2(m - m_new);  // 0 when m == -inf
+      }
       const float msub = (m_new == -INFINITY) ? 0.f : m_new;
-      // P buffer and O are free once PV_{j-1} has completed
-      if (j > 0) {
-        mbar_wait(bOReady, (j - 1) & 1);
+      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+        mbar_wait(bOReady, (j - 1) & 1);  // O holds PV_{j-1}
         tc_fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
-          const uint32_t tO = tmem + lane_base + TM_O;
+        const uint32_t tO = tmem + lane_base + TM_O;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld_32x32b_x32(tO + 32 * c, o);
-            tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(tO + 32 * c, o);
+          tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-            tmem_st_32x32b_x32(tO + 32 * c, o);
-          }
-          tmem_st_wait();
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+          tmem_st_32x32b_x32(tO + 32 * c, o);
         }
       }
-      // pass 2: P = exp2(s * scale_log2 - m_new) -> shared (K-major SW128: atom = key / 64,
-      // 16-B chunk swizzled by row); 8 independent partial sums
+      // P = exp2(s * scale_log2 - m) -> packed 16-bit pairs written back over S_j (TMEM cols 0..63)
       float sm8[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) sm8[t] = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + 32 * c, v);
-        tmem_ld_wait();
-        float pe[32];
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          pe[e] = ex2(fmaf(__uint_as_float(v[e]), p.scale_log2, -msub));
-          if (!full_block && !valid(key0 + 32 * c + e)) pe[e] = 0.f;
-          sm8[e & 7] += pe[e];
+          const float p0 = ex2(fmaf(__uint_as_float(v[64 * c + 2 * e]), p.scale_log2, -msub));
+          const float p1 = ex2(fmaf(__uint_as_float(v[64 * c + 2 * e + 1]), p.scale_log2, -msub));
+          sm8[(2 * e) & 7] += p0;
+          sm8[(2 * e + 1) & 7] += p1;
+          pk[e] = pack2<DT>(p0, p1);
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = pack2<DT>(pe[2 * e], pe[2 * e + 1]);
-        const uint32_t atom = sP + (c >> 1) * ATOM + r * 128;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int chunk = (c & 1) * 4 + u;
-          st_shared_v4(atom + ((chunk ^ (r & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
+        tmem_st_32x32b_x32(tS + 32 * c, pk);
       }
+      tmem_st_wait();
       const float sum = ((sm8[0] + sm8[1]) + (sm8[2] + sm8[3])) + ((sm8[4] + sm8[5]) + (sm8[6] + sm8[7]));
       l = l * corr + sum;
       m = m_new;
-      tc_fence_before();
-      fence_proxy_async_smem();  // P (generic stores) -> tensor core (async proxy)
+      tc_fence_before();  // P and the rescaled O (tcgen05.st) before the MMA issuer's PV_j
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(bSEmpty + 8 * s);
-        mbar_arrive(bPReady);
-      }
+      if (lane == 0) mbar_arrive(bPReady);
     }
     // ---------------------------------------------------------------- epilogue: O / l, lse
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
