@@ -3,18 +3,21 @@
 //
 //   S = scale * Q K^T,  P = softmax_rows(S) (causal: key j <= query i),  O = P V,  lse = log sum exp S
 //
-// One CTA per (128-row query tile, batch*head).  Warp roles:
+// One CTA per (two 128-row query tiles, batch*head).  Warp roles:
 //   warp 0      TMA producer: Q tile once, then K_j / V_j blocks (128 keys) into a 2-stage ring.
 //   warp 1      tcgen05.mma issuer: S_j = Q K_j^T into one of two TMEM score buffers, then
 //               O += P_j V_j into the TMEM output accumulator.  It issues S_{j+1} before waiting for
 //               P_j, so the tensor core computes the next scores while the SIMT warps run the
 //               softmax of block j -- the FA3 software pipeline expressed with two
 //               TMEM score buffers instead of a register copy.
-//   warps 2-5   softmax (thread = query row = TMEM lane): running row max / sum in the exp2 domain,
-//               P_j (fp16/bf16) into shared memory in the MMA's K-major SW128 layout, rescale of
-//               the O accumulator in TMEM when the row max grows (tcgen05.ld/st), and the final
-//               O / l normalisation + TMA store and lse.
-// TMEM: S0 [0,128) S1 [128,256) O [256,384).  Shared: Q 32 KB, K/V 2 x 64 KB, P 32 KB.
+//   warps 2-5,  softmax warpgroups for query tiles 0 and 1 (thread = query row = TMEM lane):
+//   warps 6-9   S_t read once from TMEM into registers, running row max / sum in the exp2 domain,
+//               P_t (16-bit) written back over S_t in TMEM and consumed by tcgen05.mma with A from
+//               TMEM, lazy rescale of the O_t accumulator (only when the row max grows by > 2^8),
+//               final O / l normalisation + TMA store and lse.  While one warpgroup runs its softmax
+//               the tensor core computes the other tile's S and P.V (ping-pong), and every K/V
+//               block is reused by both tiles.
+// TMEM: S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512).  Shared: Q 2 x 32 KB, K/V 2 x 64 KB.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -33,21 +36,19 @@ namespace cy_attn {
 using namespace cy;
 
 constexpr int D = 128;        // head dim (the paper's configuration)
-constexpr int BQ = 128;       // query rows per CTA (TMEM lanes)
+constexpr int BQ = 128;       // query rows per tile (TMEM lanes)
+constexpr int NT = 2;         // query tiles per CTA (two softmax warpgroups ping-pong on the tensor core)
 constexpr int BKV = 128;      // keys per block
 constexpr int ATOM = 128 * 128;            // one SW128 atom column: 128 rows x 64 elements x 2 B
 constexpr int TILE = 2 * ATOM;             // 128 rows x 128 elements
-constexpr int SQ_OFF = 0;
-constexpr int SK_OFF = TILE;               // [2]
-constexpr int SV_OFF = 3 * TILE;           // [2]
-constexpr int SP_OFF = 5 * TILE;
-constexpr int BAR_OFF = 6 * TILE;
-constexpr int SMEM_BYTES = 1024 + 6 * TILE + 256;
-constexpr int THREADS = 6 * 32;
-constexpr uint32_t TM_S0 = 0, TM_O = 256;
-
-template <int DT>
-struct Types;
+constexpr int SQ_OFF = 0;                  // [NT]
+constexpr int SK_OFF = NT * TILE;          // [2]
+constexpr int SV_OFF = (NT + 2) * TILE;    // [2]
+constexpr int BAR_OFF = (NT + 4) * TILE;
+constexpr int SMEM_BYTES = 1024 + (NT + 4) * TILE + 256;
+constexpr int THREADS = (4 * NT + 2) * 32;  // softmax warpgroups 0..NT-1, then producer, MMA issuer
+constexpr int W_PROD = 4 * NT, W_MMA = 4 * NT + 1;
+constexpr uint32_t TM_S = 0, TM_O = 256;   // S_t at 128 t, O_t at 256 + 128 t
 
 struct Params {
   int sq, sk, bh;
@@ -63,16 +64,20 @@ __host__ __device__ constexpr uint32_t idesc() {
          (uint32_t(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+template <int N>
+__device__ __forceinline__ void tmem_st_32x32b(uint32_t taddr, const uint32_t* r);
+template <>
+__device__ __forceinline__ void tmem_st_32x32b<16>(uint32_t taddr, const uint32_t* r) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
-      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  tmem_st_32x32b<16>(taddr, r);
+  tmem_st_32x32b<16>(taddr + 16, r + 16);
 }
 // D[tmem] (+)= A[tmem] * B[smem desc]: kind::f16, cta_group::1, A (K-major) read from tensor memory
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
@@ -102,6 +107,11 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
+__device__ __forceinline__ int blocks_for(const Params& p, int row_end) {
+  const int kv_end = p.causal ? min(p.sk, row_end) : p.sk;
+  return (kv_end + BKV - 1) / BKV;
+}
+
 template <int DT>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -110,21 +120,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
-  const uint32_t sQ = base + SQ_OFF, sK = base + SK_OFF, sV = base + SV_OFF, sP = base + SP_OFF;
+  const uint32_t sQ = base + SQ_OFF, sK = base + SK_OFF, sV = base + SV_OFF;
   const uint32_t bar = base + BAR_OFF;
-  const uint32_t bQFull = bar, bKVFull = bar + 8, bKVEmpty = bar + 24, bSFull = bar + 40, bSEmpty = bar + 56,
-                 bPReady = bar + 72, bOReady = bar + 80, sTmemSlot = bar + 96;
+  const uint32_t bQFull = bar, bKVFull = bar + 8, bKVEmpty = bar + 24, bSFull = bar + 40, bPReady = bar + 56,
+                 bOReady = bar + 72, sTmemSlot = bar + 88;
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heavy (long) causal tiles first
-  const int qt = p.causal ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
+  const int qt = p.causal ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;  // heavy causal CTAs first
   const int hb = blockIdx.y;
-  const int q0 = qt * BQ;
-  const int kv_end = p.causal ? min(p.sk, q0 + BQ) : p.sk;
-  const int nkv = (kv_end + BKV - 1) / BKV;
+  const int q0 = qt * BQ * NT;
+  int nkv[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) nkv[t] = blocks_for(p, q0 + BQ * (t + 1));
+  const int nall = nkv[NT - 1];  // tiles further down need at least as many blocks
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_PROD && lane == 0) {
     prefetch_tmap(&tmQ);
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
@@ -133,14 +144,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(bKVFull + 8 * s, 1);
       mbar_init(bKVEmpty + 8 * s, 1);
-      mbar_init(bSFull + 8 * s, 1);
-      mbar_init(bSEmpty + 8 * s, 4);
     }
-    mbar_init(bPReady, 4);
-    mbar_init(bOReady, 1);
+    for (int t = 0; t < NT; ++t) {
+      mbar_init(bSFull + 8 * t, 1);
+      mbar_init(bPReady + 8 * t, 4);
+      mbar_init(bOReady + 8 * t, 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) {
+  if (warp == W_MMA) {
     tmem_alloc<1>(sTmemSlot, 512);
     tmem_relinquish<1>();
   }
@@ -151,14 +163,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   pdl_wait();
   if (threadIdx.x == 0) pdl_launch_dependents();
 
-  if (warp == 0) {
+  if (warp == W_PROD) {
     // ---------------------------------------------------------------- producer
-    if (lane == 0 && nkv > 0) {
+    if (lane == 0 && nall > 0) {
       const uint64_t pol = policy_evict_last();
-      mbar_arrive_expect_tx(bQFull, TILE);
-      tma_load_3d(sQ, &tmQ, bQFull, 0, q0, hb, pol);
-      tma_load_3d(sQ + ATOM, &tmQ, bQFull, 64, q0, hb, pol);
-      for (int j = 0; j < nkv; ++j) {
+      mbar_arrive_expect_tx(bQFull, NT * TILE);
+      for (int t = 0; t < NT; ++t) {
+        tma_load_3d(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t, hb, pol);
+        tma_load_3d(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, q0 + BQ * t, hb, pol);
+      }
+      for (int j = 0; j < nall; ++j) {
         const int s = j & 1;
         mbar_wait(bKVEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(bKVFull + 8 * s, 2 * TILE);
@@ -169,79 +183,97 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_3d(sV + s * TILE + ATOM, &tmV, bKVFull + 8 * s, 64, k0, hb, pol);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0 && nkv > 0) {
+    // Tensor-core order per block j: PV_0(j) | S_0(j+1) | PV_1(j) | S_1(j+1): while one softmax
+    // warpgroup turns S_t into P_t, the tensor core runs the other tile's GEMMs (ping-pong).
+    if (lane == 0 && nall > 0) {
       constexpr uint32_t ID_S = idesc<DT, false>(), ID_PV = idesc<DT, true>();
-      auto issue_s = [&](int j) {
-        const int s = j & 1;
-        const uint32_t k = sK + s * TILE;
+      auto issue_s = [&](int t, int j) {
+        const uint32_t k = sK + (j & 1) * TILE, q = sQ + t * TILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
-          mma_f16<1>(tmem + TM_S0 + s * 128, sdesc_sw128(sQ + off, 16, 1024), sdesc_sw128(k + off, 16, 1024), ID_S,
+          mma_f16<1>(tmem + TM_S + t * 128, sdesc_sw128(q + off, 16, 1024), sdesc_sw128(k + off, 16, 1024), ID_S,
                      kk > 0);
         }
-        mma_commit<1>(bSFull + 8 * s, 0);
+        mma_commit<1>(bSFull + 8 * t, 0);
+      };
+      auto issue_pv = [&](int t, int j) {
+        mbar_wait(bPReady + 8 * t, j & 1);
+        tc_fence_after();
+        const uint32_t v = sV + (j & 1) * TILE;
+        // O_t += P_t V_j: P_t read from TMEM (packed 16-bit pairs over S_t, 8 columns per k16 step);
+        // S_t(j+1) is issued after this and tcgen05 ops execute in order, so it cannot clobber P_t.
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + kk * 8, sdesc_sw128(v + kk * 2048, ATOM, 1024),
+                     ID_PV, (j | kk) != 0);
+        mma_commit<1>(bOReady + 8 * t, 0);
       };
       mbar_wait(bQFull, 0);
       mbar_wait(bKVFull, 0);
       tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        if (j + 1 < nkv) {  // next scores while the softmax of block j runs
-          const int s1 = (j + 1) & 1;
-          mbar_wait(bKVFull + 8 * s1, ((j + 1) >> 1) & 1);
-          // S buffer s1 held P_{j-1}; PV_{j-1} was issued before this MMA and tcgen05 ops execute
-          // in issue order, so the overwrite is safe without a barrier.
+      for (int t = 0; t < NT; ++t)
+        if (nkv[t] > 0) issue_s(t, 0);
+      for (int j = 0; j < nall; ++j) {
+        const bool next = j + 1 < nall;
+        if (next) {
+          mbar_wait(bKVFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
           tc_fence_after();
-          issue_s(j + 1);
         }
-        mbar_wait(bPReady, j & 1);
-        tc_fence_after();
-        const uint32_t v = sV + s * TILE;
-        // O += P_j V_j with P_j read from TMEM (packed 16-bit pairs over the S_j buffer, 8 columns
-        // per k16 step) and V_j from shared memory (MN-major)
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_f16_ts(tmem + TM_O, tmem + TM_S0 + s * 128 + kk * 8, sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV,
-                     (j | kk) != 0);
-        mma_commit<1>(bOReady, 0);
-        mma_commit<1>(bKVEmpty + 8 * s, 0);
+        for (int t = 0; t < NT; ++t) {
+          if (j < nkv[t]) issue_pv(t, j);
+          if (t == NT - 1) mma_commit<1>(bKVEmpty + 8 * (j & 1), 0);  // K_j, V_j fully consumed
+          if (next && j + 1 < nkv[t]) issue_s(t, j + 1);
+        }
       }
     }
-  } else {
+  } else if (warp < 4 * NT) {
     // ---------------------------------------------------------------- softmax / correction / epilogue
-    const int q = warp & 3;
-    const int r = 32 * q + lane;  // query row within the tile = TMEM lane
-    const int qrow = q0 + r;
+    const int t = warp >> 2;        // query tile of this warpgroup
+    const int q = warp & 3;         // TMEM lane quarter
+    const int r = 32 * q + lane;    // row within the tile = TMEM lane
+    const int trow0 = q0 + BQ * t;
+    const int qrow = trow0 + r;
+    const int nk = nkv[t];
     const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const uint32_t tS = tmem + lane_base + TM_S + t * 128;
+    const uint32_t tO = tmem + lane_base + TM_O + t * 128;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int s = j & 1;
-      mbar_wait(bSFull + 8 * s, (j >> 1) & 1);
+    for (int j = 0; j < nk; ++j) {
+      mbar_wait(bSFull + 8 * t, j & 1);
       tc_fence_after();
-      const uint32_t tS = tmem + lane_base + TM_S0 + s * 128;
       const int key0 = j * BKV;
-      const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= q0);
-      // key validity only matters in the last (ragged) block and in the causal diagonal block
-      auto valid = [&](int key) { return full_block || (key < p.sk && (!p.causal || key <= qrow)); };
-      // S_j row -> registers (one TMEM read), masked keys -> -inf
-      uint32_t v[128];
+      const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= trow0);
+      // masked keys (ragged last block / causal diagonal) read as -inf
+      auto fix = [&](uint32_t (&v)[64], int g) {
+        if (!full_block) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * c]));
-      tmem_ld_wait();
-      if (!full_block) {
-#pragma unroll
-        for (int e = 0; e < 128; ++e)
-          if (!valid(key0 + e)) v[e] = __float_as_uint(-INFINITY);
-      }
+          for (int e = 0; e < 64; ++e) {
+            const int key = key0 + 64 * g + e;
+            if (key >= p.sk || (p.causal && key > qrow)) v[e] = __float_as_uint(-INFINITY);
+          }
+        }
+      };
+      auto load64 = [&](uint32_t (&v)[64], int g) {
+        tmem_ld_32x32b_x32(tS + 64 * g, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        tmem_ld_32x32b_x32(tS + 64 * g + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        tmem_ld_wait();
+      };
+      // pass 1 (TMEM -> registers in 64-column groups): row max, 8 independent partial maxima
       float mx8[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) mx8[t] = -INFINITY;
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 128; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+      for (int g = 0; g < 2; ++g) {
+        uint32_t v[64];
+        load64(v, g);
+        fix(v, g);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+      }
       float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;  // scale_log2 > 0 keeps the order
@@ -254,10 +286,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       const float msub = (m_new == -INFINITY) ? 0.f : m_new;
       if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
-        mbar_wait(bOReady, (j - 1) & 1);  // O holds PV_{j-1}
+        mbar_wait(bOReady + 8 * t, (j - 1) & 1);  // O_t holds PV_t(j-1)
         tc_fence_after();
-        const uint32_t tO = tmem + lane_base + TM_O;
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
           tmem_ld_32x32b_x32(tO + 32 * c, o);
@@ -267,45 +298,49 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_st_32x32b_x32(tO + 32 * c, o);
         }
       }
-      // P = exp2(s * scale_log2 - m) -> packed 16-bit pairs written back over S_j (TMEM cols 0..63)
+      // pass 2: P = exp2(s * scale_log2 - m) -> packed 16-bit pairs written back over S_t (TMEM
+      // cols 0..63; group g's 64 scores become P columns 32g..32g+31, read by the MMA afterwards)
       float sm8[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) sm8[t] = 0.f;
+      for (int u = 0; u < 8; ++u) sm8[u] = 0.f;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int g = 0; g < 2; ++g) {
+        uint32_t v[64];
+        load64(v, g);
+        fix(v, g);
         uint32_t pk[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[64 * c + 2 * e]), p.scale_log2, -msub));
-          const float p1 = ex2(fmaf(__uint_as_float(v[64 * c + 2 * e + 1]), p.scale_log2, -msub));
+          const float p0 = ex2(fmaf(__uint_as_float(v[2 * e]), p.scale_log2, -msub));
+          const float p1 = ex2(fmaf(__uint_as_float(v[2 * e + 1]), p.scale_log2, -msub));
           sm8[(2 * e) & 7] += p0;
           sm8[(2 * e + 1) & 7] += p1;
           pk[e] = pack2<DT>(p0, p1);
         }
-        tmem_st_32x32b_x32(tS + 32 * c, pk);
+        // group 1's P lands in columns 32..63, which group 1's scores (columns 64..127) do not
+        // overlap; group 0's P (columns 0..31) overwrites scores already consumed
+        tmem_st_32x32b_x32(tS + 32 * g, pk);
       }
       tmem_st_wait();
-      const float sum = ((sm8[0] + sm8[1]) + (sm8[2] + sm8[3])) + ((sm8[4] + sm8[5]) + (sm8[6] + sm8[7]));
-      l = l * corr + sum;
+      l = l * corr + (((sm8[0] + sm8[1]) + (sm8[2] + sm8[3])) + ((sm8[4] + sm8[5]) + (sm8[6] + sm8[7])));
       m = m_new;
-      tc_fence_before();  // P and the rescaled O (tcgen05.st) before the MMA issuer's PV_j
+      tc_fence_before();  // P and the rescaled O (tcgen05.st) before the MMA issuer's PV_t(j)
       __syncwarp();
-      if (lane == 0) mbar_arrive(bPReady);
+      if (lane == 0) mbar_arrive(bPReady + 8 * t);
     }
     // ---------------------------------------------------------------- epilogue: O / l, lse
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
-    if (nkv > 0) {
-      mbar_wait(bOReady, (nkv - 1) & 1);
+    if (nk > 0) {
+      mbar_wait(bOReady + 8 * t, (nk - 1) & 1);
       tc_fence_after();
     }
-    const uint32_t sE = sP + q * 4096;  // P is no longer read: 4 KB staging per warp
+    const uint32_t sE = sQ + t * TILE + q * 4096;  // Q_t is no longer read: 4 KB staging per warp
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       uint32_t a0[32], a1[32];
-      if (nkv > 0) {
-        const uint32_t tO = tmem + lane_base + TM_O + 64 * c;
-        tmem_ld_32x32b_x32(tO, a0);
-        tmem_ld_32x32b_x32(tO + 32, a1);
+      if (nk > 0) {
+        tmem_ld_32x32b_x32(tO + 64 * c, a0);
+        tmem_ld_32x32b_x32(tO + 64 * c + 32, a1);
         tmem_ld_wait();
       } else {
 #pragma unroll
@@ -328,7 +363,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_3d(&tmO, sE, 64 * c, q0 + 32 * q, hb);
+        tma_store_3d(&tmO, sE, 64 * c, trow0 + 32 * q, hb);
         bulk_commit();
       }
     }
@@ -339,7 +374,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc<1>(tmem, 512);
   }
@@ -427,7 +462,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   }
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)((seq_q + BQ - 1) / BQ), (unsigned)bh, 1);
+  cfg.gridDim = dim3((unsigned)((seq_q + BQ * NT - 1) / (BQ * NT)), (unsigned)bh, 1);
   cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = static_cast<cudaStream_t>(stream);
