@@ -26,6 +26,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -96,6 +97,17 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (offloads the MUFU unit): x = n + f, 2^f by a cubic (max rel err 8.6e-5,
+// below the 2^-11 rounding of the 16-bit P it feeds), 2^n added to the exponent field.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float n = floorf(xc);
+  const float f = xc - n;
+  const float p = fmaf(fmaf(fmaf(0.07706515491008759f, f, 0.22764705121517181f), f, 0.6951163411140442f), f, 1.f);
+  const float y = __int_as_float(__float_as_int(p) + (static_cast<int>(n) << 23));
+  return x < -126.f ? 0.f : y;
+}
+
 template <int DT>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   if constexpr (DT == 0) {
@@ -112,7 +124,7 @@ __device__ __forceinline__ int blocks_for(const Params& p, int row_end) {
   return (kv_end + BKV - 1) / BKV;
 }
 
-template <int DT>
+template <int DT, int EMU>  // EMU of every 8 exponentials are evaluated with ex2_poly
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -311,8 +323,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[2 * e]), p.scale_log2, -msub));
-          const float p1 = ex2(fmaf(__uint_as_float(v[2 * e + 1]), p.scale_log2, -msub));
+          const float x0 = fmaf(__uint_as_float(v[2 * e]), p.scale_log2, -msub);
+          const float x1 = fmaf(__uint_as_float(v[2 * e + 1]), p.scale_log2, -msub);
+          const float p0 = ((2 * e) & 7) < EMU ? ex2_poly(x0) : ex2(x0);
+          const float p1 = ((2 * e + 1) & 7) < EMU ? ex2_poly(x1) : ex2(x1);
           sm8[(2 * e) & 7] += p0;
           sm8[(2 * e + 1) & 7] += p1;
           pk[e] = pack2<DT>(p0, p1);
@@ -384,7 +398,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_attr_mu;
-bool g_attr_set[64][2] = {};
+bool g_attr_set[64][2][4] = {};
 
 bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r) {
   cuuint64_t dims[3] = {uint64_t(D), rows, bh};
@@ -449,15 +463,27 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.lse = lse;
-  const void* fn = dt == CY_F16 ? (const void*)&attn_fwd_kernel<0> : (const void*)&attn_fwd_kernel<1>;
+  // CY_ATTN_EMU: how many of every 8 exponentials run on the FMA pipe (tuning knob; default 0:
+  // measured on B200 the softmax is issue-bound, not MUFU-bound, so emulation only adds work)
+  static const int emu = [] {
+    const char* e = std::getenv("CY_ATTN_EMU");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 0;
+  }();
+  const void* fns[2][4] = {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
+                            (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
+                           {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
+                            (const void*)&attn_fwd_kernel<1, 3>, (const void*)&attn_fwd_kernel<1, 4>}};
+  const int ei = emu == 0 ? 0 : emu - 1;
+  const void* fn = fns[dt][ei];
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
-    if (!g_attr_set[dev][dt]) {
+    if (!g_attr_set[dev][dt][ei]) {
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) {
         cudaGetLastError();
         return CY_ERR_LAUNCH;
       }
-      g_attr_set[dev][dt] = true;
+      g_attr_set[dev][dt][ei] = true;
     }
   }
   cudaLaunchConfig_t cfg;
