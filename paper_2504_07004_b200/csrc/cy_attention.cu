@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "cy_ptx.cuh"
 #include "cypress_b200.h"
@@ -97,15 +98,55 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA pipe (offloads the MUFU unit): x = n + f, 2^f by a cubic (max rel err 8.6e-5,
-// below the 2^-11 rounding of the 16-bit P it feeds), 2^n added to the exponent field.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -126.f);
-  const float n = floorf(xc);
-  const float f = xc - n;
-  const float p = fmaf(fmaf(fmaf(0.07706515491008759f, f, 0.22764705121517181f), f, 0.6951163411140442f), f, 1.f);
-  const float y = __int_as_float(__float_as_int(p) + (static_cast<int>(n) << 23));
-  return x < -126.f ? 0.f : y;
+// Blackwell 2-wide fp32 SIMD (FFMA2 / FADD2): two lanes of work per issued instruction; each lane
+// rounds exactly like the scalar fma/add, so results are unchanged.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("{.reg .b64 ra, rb, rc;\n\t"
+      "mov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\tmov.b64 rc, {%5, %6};\n\t"
+      "fma.rn.f32x2 %0, ra, rb, rc;}"
+      : "=l"(d) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("{.reg .b64 ra, rb;\n\t"
+      "mov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+      "add.rn.f32x2 %0, ra, rb;}"
+      : "=l"(d) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("{.reg .b64 ra, rb;\n\t"
+      "mov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+      "sub.rn.f32x2 %0, ra, rb;}"
+      : "=l"(d) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+
+// 2^x for a pair on the FMA/ALU pipes only (no MUFU, no FRND/F2I, which issue on the XU pipe):
+// n = rint(x) by the 1.5*2^23 magic add, f = x - n in [-1/2, 1/2], 2^f by a cubic fitted for
+// minimax relative error on [-1/2, 1/2] (max 7.5e-5 in fp32, below the 2^-11 rounding of the
+// 16-bit P it feeds), then n is added to the exponent field.  x is clamped at -126, so inputs
+// below that return a value < 2^-125 instead of 0; callers only use it where no score is masked.
+__device__ __forceinline__ float2 ex2_emu2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, magic);
+  const float2 f = fsub2(x, fsub2(t, magic));
+  float2 p = ffma2(make_float2(0.05517167f, 0.05517167f), f, make_float2(0.24261112f, 0.24261112f));
+  p = ffma2(p, f, make_float2(0.69326099f, 0.69326099f));
+  p = ffma2(p, f, make_float2(0.99992807f, 0.99992807f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 template <int DT>
@@ -124,7 +165,7 @@ __device__ __forceinline__ int blocks_for(const Params& p, int row_end) {
   return (kv_end + BKV - 1) / BKV;
 }
 
-template <int DT, int EMU>  // EMU of every 8 exponentials are evaluated with ex2_poly
+template <int DT, int EMU>  // EMU of every 8 exponential pairs are evaluated with ex2_emu2
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -312,31 +353,47 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       // pass 2: P = exp2(s * scale_log2 - m) -> packed 16-bit pairs written back over S_t (TMEM
       // cols 0..63; group g's 64 scores become P columns 32g..32g+31, read by the MMA afterwards)
-      float sm8[8];
+      // sm4[u].x / .y accumulate elements 2e / 2e+1 with e % 4 == u (8 independent fp32 chains)
+      float2 sm4[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sm8[u] = 0.f;
+      for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+      const float2 ms2 = make_float2(-msub, -msub);
+      // E of every 8 pairs take the FMA-pipe exponential (only in blocks without masked scores,
+      // where ex2_emu2's clamp never applies to a -inf)
+      auto pass2 = [&](auto e_c) {
+        constexpr int E = decltype(e_c)::value;
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        uint32_t v[64];
-        load64(v, g);
-        fix(v, g);
-        uint32_t pk[32];
+        for (int g = 0; g < 2; ++g) {
+          uint32_t v[64];
+          load64(v, g);
+          if constexpr (E == 0) fix(v, g);
+          uint32_t pk[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float x0 = fmaf(__uint_as_float(v[2 * e]), p.scale_log2, -msub);
-          const float x1 = fmaf(__uint_as_float(v[2 * e + 1]), p.scale_log2, -msub);
-          const float p0 = ((2 * e) & 7) < EMU ? ex2_poly(x0) : ex2(x0);
-          const float p1 = ((2 * e + 1) & 7) < EMU ? ex2_poly(x1) : ex2(x1);
-          sm8[(2 * e) & 7] += p0;
-          sm8[(2 * e + 1) & 7] += p1;
-          pk[e] = pack2<DT>(p0, p1);
+          for (int e = 0; e < 32; ++e) {
+            const float2 x = ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sc2, ms2);
+            float2 pe;
+            if ((e & 7) < E) {
+              pe = ex2_emu2(x);
+            } else {
+              pe.x = ex2(x.x);
+              pe.y = ex2(x.y);
+            }
+            sm4[e & 3] = fadd2(sm4[e & 3], pe);
+            pk[e] = pack2<DT>(pe.x, pe.y);
+          }
+          // group 1's P lands in columns 32..63, which group 1's scores (columns 64..127) do not
+          // overlap; group 0's P (columns 0..31) overwrites scores already consumed
+          tmem_st_32x32b_x32(tS + 32 * g, pk);
         }
-        // group 1's P lands in columns 32..63, which group 1's scores (columns 64..127) do not
-        // overlap; group 0's P (columns 0..31) overwrites scores already consumed
-        tmem_st_32x32b_x32(tS + 32 * g, pk);
-      }
+      };
+      if (EMU > 0 && full_block)
+        pass2(std::integral_constant<int, EMU>{});
+      else
+        pass2(std::integral_constant<int, 0>{});
       tmem_st_wait();
-      l = l * corr + (((sm8[0] + sm8[1]) + (sm8[2] + sm8[3])) + ((sm8[4] + sm8[5]) + (sm8[6] + sm8[7])));
+      l = l * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
+                      ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
       m = m_new;
       tc_fence_before();  // P and the rescaled O (tcgen05.st) before the MMA issuer's PV_t(j)
       __syncwarp();
@@ -463,8 +520,8 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.lse = lse;
-  // CY_ATTN_EMU: how many of every 8 exponentials run on the FMA pipe (tuning knob; default 0:
-  // measured on B200 the softmax is issue-bound, not MUFU-bound, so emulation only adds work)
+  // CY_ATTN_EMU: how many of every 8 exponential pairs run on the FMA pipe (tuning knob; default 0:
+  // measured on B200 at 2/8..4/8 it is 2-5% slower -- the softmax is not MUFU-throughput-bound)
   static const int emu = [] {
     const char* e = std::getenv("CY_ATTN_EMU");
     const int v = e ? std::atoi(e) : 0;
