@@ -175,8 +175,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t base = (raw + 1023u) & ~1023u;
   const uint32_t sQ = base + SQ_OFF, sK = base + SK_OFF, sV = base + SV_OFF;
   const uint32_t bar = base + BAR_OFF;
-  const uint32_t bQFull = bar, bKVFull = bar + 8, bKVEmpty = bar + 24, bSFull = bar + 40, bPReady = bar + 56,
-                 bOReady = bar + 72, sTmemSlot = bar + 88;
+  // K and V have separate 2-slot rings: K_j is released after the last S(j), V_j after the last
+  // PV(j), so each refill starts as soon as its own readers are done
+  const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bar + 24, bVFull = bar + 40, bVEmpty = bar + 56,
+                 bSFull = bar + 72, bPReady = bar + 88, bOReady = bar + 104, sTmemSlot = bar + 120;
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -195,8 +197,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     prefetch_tmap(&tmO);
     mbar_init(bQFull, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bKVFull + 8 * s, 1);
-      mbar_init(bKVEmpty + 8 * s, 1);
+      mbar_init(bKFull + 8 * s, 1);
+      mbar_init(bKEmpty + 8 * s, 1);
+      mbar_init(bVFull + 8 * s, 1);
+      mbar_init(bVEmpty + 8 * s, 1);
     }
     for (int t = 0; t < NT; ++t) {
       mbar_init(bSFull + 8 * t, 1);
@@ -227,13 +231,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       for (int j = 0; j < nall; ++j) {
         const int s = j & 1;
-        mbar_wait(bKVEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(bKVFull + 8 * s, 2 * TILE);
         const int k0 = j * BKV;
-        tma_load_3d(sK + s * TILE, &tmK, bKVFull + 8 * s, 0, k0, hb, pol);
-        tma_load_3d(sK + s * TILE + ATOM, &tmK, bKVFull + 8 * s, 64, k0, hb, pol);
-        tma_load_3d(sV + s * TILE, &tmV, bKVFull + 8 * s, 0, k0, hb, pol);
-        tma_load_3d(sV + s * TILE + ATOM, &tmV, bKVFull + 8 * s, 64, k0, hb, pol);
+        mbar_wait(bKEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(bKFull + 8 * s, TILE);
+        tma_load_3d(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0, hb, pol);
+        tma_load_3d(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0, hb, pol);
+        mbar_wait(bVEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(bVFull + 8 * s, TILE);
+        tma_load_3d(sV + s * TILE, &tmV, bVFull + 8 * s, 0, k0, hb, pol);
+        tma_load_3d(sV + s * TILE + ATOM, &tmV, bVFull + 8 * s, 64, k0, hb, pol);
       }
     }
   } else if (warp == W_MMA) {
@@ -265,22 +271,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         mma_commit<1>(bOReady + 8 * t, 0);
       };
       mbar_wait(bQFull, 0);
-      mbar_wait(bKVFull, 0);
+      mbar_wait(bKFull, 0);
       tc_fence_after();
       for (int t = 0; t < NT; ++t)
         if (nkv[t] > 0) issue_s(t, 0);
+      mma_commit<1>(bKEmpty, 0);  // K_0 consumed
       for (int j = 0; j < nall; ++j) {
         const bool next = j + 1 < nall;
         if (next) {
-          mbar_wait(bKVFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
+          mbar_wait(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
           tc_fence_after();
         }
+        mbar_wait(bVFull + 8 * (j & 1), (j >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           if (j < nkv[t]) issue_pv(t, j);
-          if (t == NT - 1) mma_commit<1>(bKVEmpty + 8 * (j & 1), 0);  // K_j, V_j fully consumed
+          if (t == NT - 1) mma_commit<1>(bVEmpty + 8 * (j & 1), 0);  // V_j fully consumed
           if (next && j + 1 < nkv[t]) issue_s(t, j + 1);
         }
+        if (next) mma_commit<1>(bKEmpty + 8 * ((j + 1) & 1), 0);  // K_{j+1} consumed
       }
     }
   } else if (warp < 4 * NT) {
