@@ -9,8 +9,9 @@ SURVEY.md section 8(a).  No collective is on the data path (weak scaling).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
 
 Other workloads (--workload): sweep-<n> (n^3), batched (64 x 1024^3, batch-sharded),
-dual (dual-GEMM pair 8192^3), rowreduce (65536/P x 8192 x 8192 + y), allgather
-(rowreduce + NCCL all-gather of D and y, replicated result).
+dual (dual-GEMM pair 8192^3), glu (silu(A*B0)*(A*B1) 8192^3), rowreduce (65536/P x 8192 x
+8192 + y), allgather (rowreduce + NCCL all-gather of D and y, replicated result), attention
+(FA forward fp16, HeadDim 128, 2 x 16 heads x 8192, non-causal; batch-sharded).
 
 Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream, W warm-up
 steps, barrier + synchronize on both sides of exactly K timed steps, max over ranks.
@@ -30,6 +31,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fp16 GEMM TFLOP/s per B200 and % of dense tensor peak; 8-GPU aggregate"
+ATTN_METRIC = "fp16 flash-attention forward TFLOP/s (HeadDim 128, 4*b*h*s^2*d FLOP)"
+
+
+def metric_for(workload):
+    return ATTN_METRIC if workload == "attention" else METRIC
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -257,7 +263,7 @@ def make_workload(name, rank, world, device):
         W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
                  desc="GLU dual-GEMM D = silu(A*B0) * (A*B1), 8192^3 (SURVEY NEXT-3, P:1532)",
                  h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=hD0.numel() * 2,
-                 shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("dual", (A, B0, B1)),
+                 shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("glu", (A, B0, B1)),
                  kernel_flops=4.0 * m_rank * n * n)
     elif name == "dual":
         n = 8192
@@ -285,6 +291,35 @@ def make_workload(name, rank, world, device):
                  h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=2 * hD0.numel() * 2,
                  shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("dual", (A, B0, B1)),
                  kernel_flops=4.0 * m_rank * n * n)
+    elif name == "attention":
+        # FA forward, FP16, HeadDim 128, non-causal; 16 heads x 8192 tokens x batch 2
+        # (16K tokens per GPU; reading R16), batch-sharded: each rank runs its own batch slice.
+        b, h, s_len, d = 2, 16, 8192, 128
+        sets, host = [], []
+        for s_i in range(2):
+            Q, K, V = (synth.uniform((b * h, s_len, d), synth.seed_for(6, 10 * rank + 3 * s_i + t)) for t in range(3))
+            host.append((Q, K, V))
+            sets.append(tuple(up(x).view(b, h, s_len, d) for x in (Q, K, V)))
+        O = torch.empty((b, h, s_len, d), dtype=torch.float16, device=device)
+        lse = torch.empty((b, h, s_len), dtype=torch.float32, device=device)
+
+        def step(i):
+            q, k, v = sets[i % 2]
+            cy.attention(q, k, v, out=O, lse=lse)
+        hQ, hK, hV = (pinned(x).view(b, h, s_len, d) for x in host[0])
+        hO = torch.empty((b, h, s_len, d), dtype=torch.float16).pin_memory()
+
+        def e2e_step(i):
+            cy.attention(hQ.to(device, non_blocking=True), hK.to(device, non_blocking=True),
+                         hV.to(device, non_blocking=True), out=O, lse=lse)
+            hO.copy_(O, non_blocking=True)
+        fl = 4.0 * b * h * s_len * s_len * d
+        W.update(flops=fl, step=step, e2e_step=e2e_step,
+                 desc=f"FA forward fp16 HeadDim 128, non-causal, batch {b} x 16 heads x 8192 (P:1594-1636, SURVEY NEXT-4)"
+                      + (f", batch-sharded over {world}" if world > 1 else ""),
+                 h2d=3 * hQ.numel() * 2, d2h=hO.numel() * 2,
+                 shape={"batch": b * world, "heads": h, "seq": s_len, "head_dim": d, "causal": False},
+                 oracle_case=("attention", host[0][:3] + (b * h,)), kernel_flops=fl)
     else:
         raise SystemExit(f"unknown workload {name}")
     return W
@@ -314,9 +349,15 @@ def oracle_baseline(case, budget_s=12.0):
         flops = 2.0 * used * m ** 3
         return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
                 "sample": f"{used} of {L} batches of 1024^3 (full GEMMs), fp64 C oracle, {dt:.1f} s"}
+    if kind == "attention":
+        return attention_sample(*arrs, budget_s=budget_s)
     if kind == "dual":
         A, B0, B1 = arrs
         fn = lambda rows: oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows)  # noqa: E731
+        per_row = 4.0 * B0.shape[1] * A.shape[1]
+    elif kind == "glu":
+        A, B0, B1 = arrs
+        fn = lambda rows: oracle.dual_glu("f16", "silu", A, B0, B1, rows=rows)  # noqa: E731
         per_row = 4.0 * B0.shape[1] * A.shape[1]
     else:
         A, B = arrs
@@ -340,6 +381,35 @@ def oracle_baseline(case, budget_s=12.0):
     dt = time.perf_counter() - t0
     return {"value": per_row * nrows / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
             "sample": f"{nrows} of {m} rows (all columns, full K) of the same inputs, fp64 C oracle, {dt:.1f} s"}
+
+
+def attention_sample(Q, K, V, bh, budget_s=12.0, rng=None):
+    """Time the fp64 oracle's attention, as it stands, on query rows sampled from one head.
+    Each sampled row costs 4*sk*d FLOP (scores + P.V), the same work per row as the kernel."""
+    import numpy as np
+
+    import oracle
+
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    nth = oracle.num_threads()
+    sq, d = Q.shape[1], Q.shape[2]
+    sk = K.shape[1]
+    per_row = 4.0 * sk * d
+    rng = rng or np.random.default_rng(0)
+
+    def run(nrows):
+        hsel = int(rng.integers(0, bh))
+        rows = np.sort(rng.choice(sq, nrows, replace=False))
+        t0 = time.perf_counter()
+        oracle.attention("f16", np.ascontiguousarray(Q[hsel:hsel + 1, rows]), K[hsel:hsel + 1], V[hsel:hsel + 1])
+        return time.perf_counter() - t0
+
+    probe = max(2 * nth, 8)
+    dt0 = run(probe)
+    nrows = int(min(sq, max(probe, probe * budget_s / max(dt0, 1e-3))))
+    dt = run(nrows)
+    return {"value": per_row * nrows / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
+            "sample": f"{nrows} random query rows of one head (all {sk} keys, HeadDim {d}), fp64 C oracle, {dt:.1f} s"}
 
 
 # ----------------------------------------------------------------------------- main
@@ -487,16 +557,19 @@ def main():
         cpu = oracle_baseline(W["oracle_case"])
 
     if rank == 0:
-        kinfo = cy.last_kernel_info()
+        kinfo = cy.last_kernel_info() if args.workload != "attention" else None
         out = {
-            "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "metric": metric_for(args.workload), "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
             "config": {"workload": W["desc"], **W["shape"],
-                       "parallelism": f"M-row shards x{world}, B replicated, no collective" if args.workload != "allgather" else f"M-row shards x{world} + NCCL all-gather",
+                       "parallelism": (f"batch shards x{world}, no collective" if args.workload in ("batched", "attention")
+                                       else f"M-row shards x{world}, B replicated, no collective" if args.workload != "allgather"
+                                       else f"M-row shards x{world} + NCCL all-gather"),
                        "l2": "inputs rotate over 2 sets (> 126 MB L2 total)" if W["flops"] > 1e12 or args.workload == "batched" else "inputs rotate over 2 sets",
-                       "kernel_config": kinfo},
+                       "kernel_config": (kinfo if args.workload != "attention" else
+                                         "attn_fwd_kernel: 2 x 128-row query tiles per CTA, 128-key blocks, TMEM S/P/O, 10 warps")},
             "pct_of_dense_peak": round(100.0 * value / world / peak, 2),
             "pct_of_nominal_2250": round(100.0 * value / world / 2250.0, 2),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
@@ -563,27 +636,36 @@ def reference_arm(args, rank, world):
         desc = "batched fp16 GEMM 64 x 1024^3"
     elif name == "glu":
         n = 8192
-        m_rank = n // world if world > 1 else n
-        A = synth.uniform((m_rank, n), synth.seed_for(3, 10 * rank))
+        A = synth.uniform((n, n), synth.seed_for(3, 0))
         B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
         B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
-        dA, dB0, dB1 = up(A), up(B0), up(B1)
-        D0 = torch.empty((m_rank, n), dtype=torch.float16, device=device)
-
-        def step(i):
-            cy.dual_gemm_glu(dA, dB0, dB1, act="silu", out=D0)
-        hA, hB0, hB1 = pinned(A), pinned(B0), pinned(B1)
-        hD0 = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
-
-        def e2e_step(i):
-            cy.dual_gemm_glu(hA.to(device, non_blocking=True), hB0.to(device, non_blocking=True),
-                             hB1.to(device, non_blocking=True), act="silu", out=D0)
-            hD0.copy_(D0, non_blocking=True)
-        W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
-                 desc="GLU dual-GEMM D = silu(A*B0) * (A*B1), 8192^3 (SURVEY NEXT-3, P:1532)",
-                 h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=hD0.numel() * 2,
-                 shape={"m": m_rank * world, "n": n, "k": n}, oracle_case=("dual", (A, B0, B1)),
-                 kernel_flops=4.0 * m_rank * n * n)
+        per_row = 4.0 * n * n
+        m = n
+        fn = lambda rows: oracle.dual_glu("f16", "silu", A, B0, B1, rows=rows)  # noqa: E731
+        desc = "GLU dual-GEMM silu(A*B0)*(A*B1) 8192^3"
+    elif name == "attention":
+        bsz, h, s_len, d = 2, 16, 8192, 128
+        Q, K, V = (synth.uniform((bsz * h, s_len, d), synth.seed_for(6, t)) for t in range(3))
+        desc = f"FA forward fp16 HeadDim 128, non-causal, batch {bsz} x {h} heads x {s_len}"
+        steps = min(args.steps, 10)
+        warm = min(args.warmup, 3)
+        rng = np.random.default_rng(0)
+        for _ in range(warm):
+            attention_sample(Q, K, V, bsz * h, budget_s=1.0, rng=rng)
+        t0 = time.perf_counter()
+        vals = [attention_sample(Q, K, V, bsz * h, budget_s=2.0, rng=rng) for _ in range(steps)]
+        dt = time.perf_counter() - t0
+        value = statistics.mean(v["value"] for v in vals)
+        out = {"impl": "reference", "metric": ATTN_METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+               "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
+               "config": {"workload": desc, "parallelism": "CPU oracle, rank 0 only"},
+               "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": vals[0]["cores"], "kind": "oracle",
+                                "sample": f"per step: {vals[0]['sample']}"},
+               "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
     elif name == "dual":
         n = 8192
         A = synth.uniform((n, n), synth.seed_for(3, 0))

@@ -34,6 +34,10 @@
 #include "cy_ptx.cuh"
 #include "cypress_b200.h"
 
+namespace cy_internal {
+void note_launch();  // cy_gemm.cu: the library-wide launch counter behind cy_launch_count()
+}
+
 namespace cy_attn {
 using namespace cy;
 
@@ -569,5 +573,6 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     cudaGetLastError();
     return CY_ERR_LAUNCH;
   }
+  cy_internal::note_launch();
   return CY_OK;
 }

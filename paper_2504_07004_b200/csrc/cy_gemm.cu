@@ -386,6 +386,11 @@ bool ld_ok(int64_t ld) { return ld > 0 && (ld % 8) == 0; }
 
 }  // namespace
 
+// shared with the attention entry point (cy_attention.cu): every kernel this library launches
+namespace cy_internal {
+void note_launch() { g_launches.fetch_add(1); }
+}  // namespace cy_internal
+
 // ============================================================================================
 extern "C" {
 

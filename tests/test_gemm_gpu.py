@@ -605,6 +605,14 @@ def test_attention_closed_forms():
     assert_bits_equal(to_bits(O1).reshape(2, 7, d), np.repeat(V[:, :1], 7, axis=1), "one key")
 
 
+def test_attention_counts_one_launch():
+    Q, K, V = _attn_inputs(1, 2, 256, 256, seed=255)
+    n0 = cy.launch_count()
+    cy.attention(*(to_dev(x, "f16").view(1, 2, 256, 128) for x in (Q, K, V)))
+    torch.cuda.synchronize()
+    assert cy.launch_count() - n0 == 1
+
+
 def test_attention_large_sampled():
     """FA benchmark shape (16 heads x 4096, HeadDim 128), non-causal, oracle on sampled query rows."""
     b, h, s = 1, 16, 4096
