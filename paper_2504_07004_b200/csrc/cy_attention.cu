@@ -465,20 +465,352 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+
+// ============================================================================ CTA-pair kernel
+// Two CTAs of a cluster own 256 consecutive query rows of one (batch, head), 128 rows each, and
+// issue every MMA as one cta_group::2 instruction (M = 256): the leader's MMA thread computes
+//   S(j) = Q K_j^T  into a double-buffered score tile (TMEM S[j % 2]) of both CTAs, and
+//   O   += P(j) V_j with P read from TMEM columns of its own (not aliased with S).
+// K_j and V_j are split between the pair (each CTA loads 64 keys of K_j and 64 columns of V_j),
+// so every byte of K/V in shared memory serves 256 query rows, as in the two-tile kernel above.
+// Because P has its own columns and S is double-buffered, S(j+2) is issued as soon as both CTAs'
+// softmax warps have read S(j) -- the tensor core computes the next scores and the previous P.V
+// while the SIMT warps run the softmax of block j (the FA3 overlap, without the
+// S -> P -> PV -> S chain of the single-buffered layout).
+//
+// Warps 0-7: softmax.  Warp w owns TMEM lanes 32 (w % 4) .. +31 (= query rows) and score columns
+// [64 (w / 4), +64): each thread holds 64 scores of its row; the two halves of a row combine their
+// maxima through shared memory (64-thread named barrier).  Warp 8: TMA producer.  Warp 9: MMA.
+// TMEM (each CTA): S0 [0,128) S1 [128,256) O [256,384) P [384,448).
+namespace pr {
+constexpr int KS = 4, VS = 4;                   // K / V ring depths
+constexpr int Q_BYTES = 128 * 128 * 2;          // this CTA's 128 query rows (two 64-column atoms)
+constexpr int QATOM = 128 * 128;                // 128 rows x 64 elements x 2 B
+constexpr int KATOM = 64 * 128;                 // 64 keys x 64 elements x 2 B
+constexpr int K_BYTES = 2 * KATOM;              // this CTA's 64 keys x 128
+constexpr int V_BYTES = 128 * 128;              // 128 keys x this CTA's 64 columns
+constexpr int OFF_Q = 0, OFF_K = Q_BYTES, OFF_V = OFF_K + KS * K_BYTES, OFF_BAR = OFF_V + VS * V_BYTES;
+constexpr int OFF_X = OFF_BAR + 512;            // row-max exchange [2 parities][4 parts][128], l [4][128]
+constexpr int SMEM_BYTES = 1024 + OFF_X + (2 * 4 * 128 + 4 * 128) * 4;
+// NS = number of softmax warps sharing one row (column split): 2 (64 columns each) or 4 (32 each)
+template <int NS> constexpr int threads() { return (4 * NS + 2) * 32; }
+constexpr uint32_t T_S = 0, T_O = 256, T_P = 384;
+
+template <int DT, bool B_MN>
+__host__ __device__ constexpr uint32_t idesc() {  // M = 256 (cta pair), N = 128, f32 accumulate
+  return (1u << 4) | (uint32_t(DT) << 7) | (uint32_t(DT) << 10) | ((B_MN ? 1u : 0u) << 16) |
+         (uint32_t(128 >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+}
+// O[tmem] (+)= P[tmem] * V[smem desc], cta_group::2
+__device__ __forceinline__ void mma_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+}  // namespace pr
+
+template <int DT, int EMU, int NS>
+__global__ void __launch_bounds__(pr::threads<NS>(), 1)
+    attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                     const Params p) {
+  using namespace pr;
+  constexpr int W_PROD = 4 * NS, W_MMA = 4 * NS + 1;
+  constexpr int COLS = 128 / NS;  // score / output columns per softmax thread
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sQ = base + OFF_Q, sK = base + OFF_K, sV = base + OFF_V;
+  const uint32_t bar = base + OFF_BAR;
+  const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bKFull + 8 * KS, bVFull = bKEmpty + 8 * KS,
+                 bVEmpty = bVFull + 8 * VS, bSFull = bVEmpty + 8 * VS, bSFree = bSFull + 16, bPFull = bSFree + 16,
+                 bPVDone = bPFull + 8, sTmemSlot = bPVDone + 8;
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int npairs = gridDim.x >> 1;
+  const int pi = p.causal ? (npairs - 1 - int(blockIdx.x >> 1)) : int(blockIdx.x >> 1);  // heavy first
+  const int hb = blockIdx.y;
+  const int q0 = pi * 2 * BQ;                 // the pair's first query row
+  const int trow0 = q0 + BQ * int(rank);      // this CTA's first query row
+  const int n = blocks_for(p, q0 + 2 * BQ);   // key blocks the pair processes (both CTAs)
+
+  if (warp == W_PROD && lane == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    prefetch_tmap(&tmO);
+    mbar_init(bQFull, 1);
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(bKFull + 8 * s, 1);
+      mbar_init(bKEmpty + 8 * s, 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(bVFull + 8 * s, 1);
+      mbar_init(bVEmpty + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bSFull + 8 * b, 1);
+      mbar_init(bSFree + 8 * b, 2 * 4 * NS);  // every softmax warp of both CTAs
+    }
+    mbar_init(bPFull, 2 * 4 * NS);
+    mbar_init(bPVDone, 1);
+    fence_mbar_init();
+  }
+  if (warp == W_MMA) {
+    tmem_alloc<2>(sTmemSlot, 512);
+    tmem_relinquish<2>();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  if (threadIdx.x == 0) pdl_launch_dependents();
+
+  if (warp == W_PROD) {
+    // ---------------------------------------------------------------- producer (both CTAs)
+    // Every load completes on the leader's barrier (cta_group::2 TMA); the leader arms each
+    // barrier with the bytes of both CTAs.  Empty barriers are local (multicast MMA commits).
+    if (lane == 0 && n > 0) {
+      const uint64_t pol = policy_evict_last();
+      if (rank == 0) mbar_arrive_expect_tx(bQFull, 2 * Q_BYTES);
+      const uint32_t qb = mapa(bQFull, 0);
+      tma_load_3d_pair(sQ, &tmQ, qb, 0, trow0, hb, pol);
+      tma_load_3d_pair(sQ + QATOM, &tmQ, qb, 64, trow0, hb, pol);
+      for (int j = 0; j < n; ++j) {
+        const int ks = j % KS, vs = j % VS;
+        mbar_wait(bKEmpty + 8 * ks, ((j / KS) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(bKFull + 8 * ks, 2 * K_BYTES);
+        const uint32_t kb = mapa(bKFull + 8 * ks, 0);
+        const int key0 = j * BKV + 64 * int(rank);
+        tma_load_3d_pair(sK + ks * K_BYTES, &tmK, kb, 0, key0, hb, pol);
+        tma_load_3d_pair(sK + ks * K_BYTES + KATOM, &tmK, kb, 64, key0, hb, pol);
+        mbar_wait(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(bVFull + 8 * vs, 2 * V_BYTES);
+        tma_load_3d_pair(sV + vs * V_BYTES, &tmV, mapa(bVFull + 8 * vs, 0), 64 * int(rank), j * BKV, hb, pol);
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ---------------------------------------------------------------- MMA issuer (leader only)
+    if (lane == 0 && rank == 0 && n > 0) {
+      constexpr uint32_t ID_S = pr::idesc<DT, false>(), ID_PV = pr::idesc<DT, true>();
+      auto issue_s = [&](int j) {
+        const int ks = j % KS;
+        mbar_wait(bKFull + 8 * ks, (j / KS) & 1);
+        tc_fence_after();
+        const uint32_t k = sK + ks * K_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_f16<2>(tmem + T_S + (j & 1) * 128, sdesc_sw128(sQ + (kk >> 2) * QATOM + (kk & 3) * 32, 16, 1024),
+                     sdesc_sw128(k + (kk >> 2) * KATOM + (kk & 3) * 32, 16, 1024), ID_S, kk > 0);
+        mma_commit<2>(bSFull + 8 * (j & 1), 0x3);
+        mma_commit<2>(bKEmpty + 8 * ks, 0x3);
+      };
+      auto issue_pv = [&](int j) {
+        mbar_wait(bPFull, j & 1);
+        const int vs = j % VS;
+        mbar_wait(bVFull + 8 * vs, (j / VS) & 1);
+        tc_fence_after();
+        const uint32_t v = sV + vs * V_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts_pair(tmem + T_O, tmem + T_P + kk * 8, sdesc_sw128(v + kk * 2048, V_BYTES, 1024), ID_PV,
+                      (j | kk) != 0);
+        mma_commit<2>(bPVDone, 0x3);
+        mma_commit<2>(bVEmpty + 8 * vs, 0x3);
+      };
+      mbar_wait(bQFull, 0);
+      tc_fence_after();
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int j = 0; j < n; ++j) {
+        if (j + 2 < n) {  // S buffer j % 2 is free once both CTAs' softmax warps have read S(j)
+          mbar_wait(bSFree + 8 * (j & 1), (j >> 1) & 1);
+          tc_fence_after();
+          issue_s(j + 2);
+        }
+        issue_pv(j);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax / epilogue
+    const int h = warp >> 2;        // column part (of NS)
+    const int q = warp & 3;         // TMEM lane quarter
+    const int r = 32 * q + lane;    // row within this CTA's tile = TMEM lane
+    const int qrow = trow0 + r;
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const uint32_t tS = tmem + lane_base + T_S + COLS * h;
+    const uint32_t tO = tmem + lane_base + T_O + COLS * h;
+    const uint32_t tP = tmem + lane_base + T_P + (COLS / 2) * h;
+    float* xmax = reinterpret_cast<float*>(smem_raw + (base + OFF_X - raw));
+    float* xl = xmax + 2 * NS * BQ;
+    const uint32_t bar_id = 1 + q;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * NS) : "memory"); };
+    const uint32_t sfree_leader = mapa(bSFree, 0), pfull_leader = mapa(bPFull, 0);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const int b = j & 1;
+      mbar_wait(bSFull + 8 * b, (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[COLS];
+#pragma unroll
+      for (int c = 0; c < COLS / 32; ++c)
+        tmem_ld_32x32b_x32(tS + 128 * b + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * c]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(sfree_leader + 8 * b);  // S(j) is in registers
+      const int key0 = j * BKV + COLS * h;
+      const bool full_block = (j * BKV + BKV <= p.sk) && (!p.causal || j * BKV + BKV - 1 <= trow0);
+      if (!full_block) {  // masked keys (ragged last block / causal diagonal) read as -inf
+#pragma unroll
+        for (int e = 0; e < COLS; ++e) {
+          const int key = key0 + e;
+          if (key >= p.sk || (p.causal && key > qrow)) v[e] = __float_as_uint(-INFINITY);
+        }
+      }
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < COLS; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+      const float mh = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      float* xm = xmax + b * NS * BQ;
+      xm[h * BQ + r] = mh;
+      pair_sync();
+      float mb = xm[r];  // every part combines the NS maxima in the same order
+#pragma unroll
+      for (int u = 1; u < NS; ++u) mb = fmaxf(mb, xm[u * BQ + r]);
+      mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;  // scale_log2 > 0 keeps the order
+      // lazy rescaling (see the two-tile kernel): both halves see the same mb and decide alike
+      float m_new = m, corr = 1.f;
+      if (mb > m + 8.f) {
+        m_new = mb;
+        corr = ex2(m - m_new);  // 0 when m == -inf
+      }
+      const float msub = (m_new == -INFINITY) ? 0.f : m_new;
+      float2 sm4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+      const float2 ms2 = make_float2(-msub, -msub);
+      uint32_t pk[COLS / 2];
+      auto exps = [&](auto e_c) {
+        constexpr int E = decltype(e_c)::value;
+#pragma unroll
+        for (int e = 0; e < COLS / 2; ++e) {
+          const float2 x = ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sc2, ms2);
+          float2 pe;
+          if ((e & 7) < E) {
+            pe = ex2_emu2(x);
+          } else {
+            pe.x = ex2(x.x);
+            pe.y = ex2(x.y);
+          }
+          sm4[e & 3] = fadd2(sm4[e & 3], pe);
+          pk[e] = pack2<DT>(pe.x, pe.y);
+        }
+      };
+      if (EMU > 0 && full_block)
+        exps(std::integral_constant<int, EMU>{});
+      else
+        exps(std::integral_constant<int, 0>{});
+      if (j > 0) {  // PV(j-1) done: P may be overwritten and O is stable for the rescale
+        mbar_wait(bPVDone, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < COLS / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x32(tO + 32 * c, o);
+          }
+        }
+      }
+      if constexpr (COLS == 64) tmem_st_32x32b_x32(tP, pk);
+      else tmem_st_32x32b<16>(tP, pk);
+      tmem_st_wait();
+      l = l * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
+                      ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
+      m = m_new;
+      tc_fence_before();  // P and the rescaled O before the leader's PV(j)
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(pfull_leader);
+    }
+    // ---------------------------------------------------------------- epilogue: O / l, lse
+    xl[h * BQ + r] = l;
+    pair_sync();
+    float lt = xl[r];  // same order in every part
+#pragma unroll
+    for (int u = 1; u < NS; ++u) lt += xl[u * BQ + r];
+    const float inv_l = (lt > 0.f) ? 1.f / lt : 0.f;
+    if (n > 0) {
+      mbar_wait(bPVDone, (n - 1) & 1);
+      tc_fence_after();
+    }
+    // staging: 32 rows x COLS columns per warp (COLS = 64: SW128 rows; COLS = 32: plain 64-B rows)
+    const uint32_t sE = sQ + (h * 4 + q) * (32 * COLS * 2);  // Q is no longer read (all MMAs are done)
+    uint32_t a[COLS];
+    if (n > 0) {
+#pragma unroll
+      for (int c = 0; c < COLS / 32; ++c) tmem_ld_32x32b_x32(tO + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&a[32 * c]));
+      tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int e = 0; e < COLS; ++e) a[e] = 0u;
+    }
+#pragma unroll
+    for (int vv = 0; vv < COLS / 8; ++vv) {
+      uint32_t w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        w[u] = pack2<DT>(__uint_as_float(a[8 * vv + 2 * u]) * inv_l, __uint_as_float(a[8 * vv + 2 * u + 1]) * inv_l);
+      if constexpr (COLS == 64) st_shared_v4(sE + lane * 128 + ((vv ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+      else st_shared_v4(sE + lane * 64 + (vv << 4), w[0], w[1], w[2], w[3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&tmO, sE, COLS * h, trow0 + 32 * q, hb);
+      bulk_commit();
+    }
+    if (h == 0 && p.lse && qrow < p.sq)
+      p.lse[(size_t)hb * p.sq + qrow] = (lt > 0.f) ? (m + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
+    if (lane == 0) bulk_wait_read<0>();
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();  // the peer's smem / TMEM are operands of the leader's MMAs until here
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc<2>(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------------------------------ host
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_attr_mu;
-bool g_attr_set[64][2][4] = {};
+bool g_attr_set[64][3][2][4] = {};
 
-bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r) {
+bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r,
+              bool swizzle = true) {
   cuuint64_t dims[3] = {uint64_t(D), rows, bh};
   cuuint64_t strides[2] = {uint64_t(D) * 2, rows * uint64_t(D) * 2};
   cuuint32_t box[3] = {box_c, box_r, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return g_encode(m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                   const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -521,11 +853,24 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   });
   if (!g_encode) return CY_ERR_INTERNAL;
+  // Variant knobs, read per call (tests switch them in-process):
+  // CY_ATTN_KERNEL: 1 (default) the two-tile single-CTA kernel, 2 the CTA-pair kernel;
+  // CY_ATTN_SPLIT: softmax warps per row group in the pair kernel, 2 (default) or 4.
+  const int kern = [] {
+    const char* e = std::getenv("CY_ATTN_KERNEL");
+    return (e && std::atoi(e) == 2) ? 2 : 1;
+  }();
+  const int split = [] {
+    const char* e = std::getenv("CY_ATTN_SPLIT");
+    return (e && std::atoi(e) == 4) ? 4 : 2;
+  }();
   CUtensorMap tQ, tK, tV, tO;
   std::memset(&tK, 0, sizeof(tK));
   tV = tK;
-  bool ok = make_map(&tQ, dt, Q, seq_q, bh, 64, 128) && make_map(&tO, dt, O, seq_q, bh, 64, 32);
-  if (seq_k > 0) ok = ok && make_map(&tK, dt, K, seq_k, bh, 64, 128) && make_map(&tV, dt, V, seq_k, bh, 64, 128);
+  const bool o32 = kern == 2 && split == 4;  // 32-column output boxes, unswizzled staging
+  bool ok = make_map(&tQ, dt, Q, seq_q, bh, 64, 128) && make_map(&tO, dt, O, seq_q, bh, o32 ? 32 : 64, 32, !o32);
+  if (seq_k > 0)
+    ok = ok && make_map(&tK, dt, K, seq_k, bh, 64, kern == 2 ? 64 : 128) && make_map(&tV, dt, V, seq_k, bh, 64, 128);
   if (!ok) return CY_ERR_LAUNCH;
   Params p;
   p.sq = (int)seq_q;
@@ -534,40 +879,63 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.lse = lse;
-  // CY_ATTN_EMU: how many of every 8 exponential pairs run on the FMA pipe (tuning knob; default 0:
-  // measured on B200 at 2/8..4/8 it is 2-5% slower -- the softmax is not MUFU-throughput-bound)
-  static const int emu = [] {
+  // CY_ATTN_EMU: how many of every 8 exponential pairs run on the FMA pipe (tuning knob; default 0).
+  // Measured on B200 (scripts/mufu_probe.cu): MUFU.EX2 16/clk/SM, FFMA2 ~56 pairs/clk/SM (half
+  // rate), so a cubic exp2 costs about as much FMA-pipe time as MUFU time: at most +12% on the
+  // isolated softmax step and 2-5% slower inside both kernels.
+  const int emu = [] {
     const char* e = std::getenv("CY_ATTN_EMU");
     const int v = e ? std::atoi(e) : 0;
     return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 0;
   }();
-  const void* fns[2][4] = {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
-                            (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
-                           {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
-                            (const void*)&attn_fwd_kernel<1, 3>, (const void*)&attn_fwd_kernel<1, 4>}};
+  const void* fns[3][2][4] = {
+      {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
+        (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
+       {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
+        (const void*)&attn_fwd_kernel<1, 3>, (const void*)&attn_fwd_kernel<1, 4>}},
+      {{(const void*)&attn_pair_kernel<0, 0, 2>, (const void*)&attn_pair_kernel<0, 2, 2>,
+        (const void*)&attn_pair_kernel<0, 3, 2>, (const void*)&attn_pair_kernel<0, 4, 2>},
+       {(const void*)&attn_pair_kernel<1, 0, 2>, (const void*)&attn_pair_kernel<1, 2, 2>,
+        (const void*)&attn_pair_kernel<1, 3, 2>, (const void*)&attn_pair_kernel<1, 4, 2>}},
+      {{(const void*)&attn_pair_kernel<0, 0, 4>, (const void*)&attn_pair_kernel<0, 2, 4>,
+        (const void*)&attn_pair_kernel<0, 3, 4>, (const void*)&attn_pair_kernel<0, 4, 4>},
+       {(const void*)&attn_pair_kernel<1, 0, 4>, (const void*)&attn_pair_kernel<1, 2, 4>,
+        (const void*)&attn_pair_kernel<1, 3, 4>, (const void*)&attn_pair_kernel<1, 4, 4>}}};
   const int ei = emu == 0 ? 0 : emu - 1;
-  const void* fn = fns[dt][ei];
+  const int ki = kern == 1 ? 0 : (split == 2 ? 1 : 2);
+  const void* fn = fns[ki][dt][ei];
+  const int smem = kern == 2 ? pr::SMEM_BYTES : SMEM_BYTES;
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
-    if (!g_attr_set[dev][dt][ei]) {
-      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) {
+    if (!g_attr_set[dev][ki][dt][ei]) {
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return CY_ERR_LAUNCH;
       }
-      g_attr_set[dev][dt][ei] = true;
+      g_attr_set[dev][ki][dt][ei] = true;
     }
   }
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)((seq_q + BQ * NT - 1) / (BQ * NT)), (unsigned)bh, 1);
-  cfg.blockDim = dim3(THREADS, 1, 1);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  if (kern == 2) {
+    cfg.gridDim = dim3((unsigned)(2 * ((seq_q + 2 * BQ - 1) / (2 * BQ))), (unsigned)bh, 1);
+    cfg.blockDim = dim3(split == 2 ? pr::threads<2>() : pr::threads<4>(), 1, 1);
+    attrs[1].id = cudaLaunchAttributeClusterDimension;
+    attrs[1].val.clusterDim.x = 2;
+    attrs[1].val.clusterDim.y = 1;
+    attrs[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+  } else {
+    cfg.gridDim = dim3((unsigned)((seq_q + BQ * NT - 1) / (BQ * NT)), (unsigned)bh, 1);
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.numAttrs = 1;
+  }
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
   void* args[] = {&tQ, &tK, &tV, &tO, &p};
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) {
     cudaGetLastError();
