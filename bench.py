@@ -421,6 +421,7 @@ def main():
     ap.add_argument("--workload", default="gemm")
     ap.add_argument("--impl", default="cypress_b200", choices=["cypress_b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, default=-1, help="force a GEMM config id (tuning; default: heuristic)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true",
                     help="capture the K timed steps in a CUDA graph and time its replay (no host launch gaps)")
@@ -449,6 +450,8 @@ def main():
             dist.init_process_group(backend)
     import paper_2504_07004_b200 as cy
 
+    if args.config >= 0:
+        cy.force_config(args.config)
     W = make_workload(args.workload, rank, world, device)
     stream = torch.cuda.current_stream()
 

@@ -140,8 +140,9 @@ const char* cy_status_string(cy_status_t s);
 
 /* Number of compiled kernel configurations (tile shape x CTA-pairing x stages). */
 int cy_num_configs(void);
-/* Describe config `id`: writes cta_group (1|2), tile_m, tile_n, stages. Returns CY_OK or
- * CY_ERR_INVALID_VALUE. */
+/* Describe config `id`: writes cta_group (1|2), tile_m (rows per cluster tile: 128 x cta_group x
+ * CTA pairs sharing B; the last config is two pairs with B multicast, tile_m = 512), tile_n,
+ * stages. Returns CY_OK or CY_ERR_INVALID_VALUE. */
 cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int* stages);
 /* Force config `id` for subsequent GEMM / batched / rowreduce calls of this process
  * (-1 restores the shape heuristic).  Used by config-invariance tests. */

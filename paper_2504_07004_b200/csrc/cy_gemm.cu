@@ -24,19 +24,20 @@ using cy::Params;
 // ------------------------------------------------------------------------------------------
 // kernel menu
 struct KDesc {
-  int var, dt, cg, bn, stages, threads, smem;  // bn = output tile width (TILE_N)
+  int var, dt, cg, bn, stages, threads, smem, mc;  // bn = output tile width (TILE_N); mc = pairs sharing B
   const void* fn;
 };
 
-template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1>
+template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1, int MC = 1>
 KDesc kdesc() {
-  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB>;
-  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, (const void*)&cy::cy_sm100_kernel<C>};
+  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB, MC>;
+  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, (const void*)&cy::cy_sm100_kernel<C>};
 }
 
-// Shapes (cta_group, tile N) offered per variant; the GEMM menu defines the public config ids.
-struct Shape { int cg, bn; };
-constexpr Shape kGemmMenu[] = {{2, 256}, {2, 128}, {1, 256}, {1, 128}, {1, 64}, {2, 512}};
+// Shapes (cta_group, tile N, pairs per cluster) offered per variant; the GEMM menu defines the
+// public config ids.
+struct Shape { int cg, bn, mc; };
+constexpr Shape kGemmMenu[] = {{2, 256, 1}, {2, 128, 1}, {1, 256, 1}, {1, 128, 1}, {1, 64, 1}, {2, 512, 1}, {2, 512, 2}};
 constexpr int kNumGemmCfg = sizeof(kGemmMenu) / sizeof(kGemmMenu[0]);
 
 template <int DT>
@@ -47,6 +48,7 @@ void add_all(std::vector<KDesc>& v) {
   v.push_back(kdesc<DT, 1, 128, 6, cy::V_GEMM>());
   v.push_back(kdesc<DT, 1, 64, 8, cy::V_GEMM>());
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2>());
+  v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2, 2>());
   v.push_back(kdesc<DT, 2, 256, 6, cy::V_ROWREDUCE>());
   v.push_back(kdesc<DT, 2, 128, 8, cy::V_ROWREDUCE>());
   v.push_back(kdesc<DT, 1, 128, 6, cy::V_ROWREDUCE>());
@@ -118,6 +120,7 @@ struct DevState {
   bool ok = false;
   int sms = 0;
   std::vector<char> attr_set;  // per menu entry: max dynamic smem attribute applied
+  std::vector<int> max_clusters;  // per menu entry: co-resident clusters (0 = not queried yet)
 };
 std::mutex g_mu;
 DevState g_dev[64];
@@ -135,6 +138,7 @@ cy_status_t device_state(int& dev, DevState*& st) {
     cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev);
     st->ok = (major == 10 && minor == 0);
     st->attr_set.assign(menu().size(), 0);
+    st->max_clusters.assign(menu().size(), 0);
     if (!g_encode) {
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q;
@@ -255,13 +259,14 @@ int pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms) {
   if (forced >= 0 && forced < kNumGemmCfg) {
     for (size_t i = 0; i < mn.size(); ++i)
       if (mn[i].var == var && mn[i].dt == dt && mn[i].cg == kGemmMenu[forced].cg &&
-          mn[i].bn == kGemmMenu[forced].bn)
+          mn[i].bn == kGemmMenu[forced].bn && mn[i].mc == kGemmMenu[forced].mc)
         return static_cast<int>(i);
   }
   int best = -1;
   double best_cost = 0;
   for (size_t i = 0; i < mn.size(); ++i) {
     if (mn[i].var != var || mn[i].dt != dt) continue;
+    if (mn[i].mc != 1) continue;  // B-multicast clusters: only when forced (being evaluated)
     const bool dual = (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM || var == cy::V_DUAL_GLU);
     const int acc_cols = ((var == cy::V_DUAL_PAIR || var == cy::V_DUAL_GLU) ? 2 : 1) * mn[i].bn;
     (void)dual;
@@ -290,7 +295,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   const int idx = pick(var, dt, m, n, k, L, st->sms);
   if (idx < 0) return CY_ERR_INTERNAL;
   const KDesc& kd = menu()[idx];
-  const int bm = 128 * kd.cg;
+  const int bm = 128 * kd.cg * kd.mc;  // rows per cluster tile
   const int bn_cta = kd.bn / kd.cg;
 
   CUtensorMap tA, tB0, tB1, tC0, tC1, tD0, tD1;
@@ -347,7 +352,29 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
       st->attr_set[idx] = 1;
     }
   }
-  const int units = std::max(1, st->sms / kd.cg);
+  const int csize = kd.cg * kd.mc;
+  if (kd.mc > 1 && st->max_clusters[idx] == 0) {  // clusters of 4 do not tile every GPC: ask
+    cudaLaunchConfig_t q;
+    std::memset(&q, 0, sizeof(q));
+    q.gridDim = dim3(csize * 256, 1, 1);
+    q.blockDim = dim3(kd.threads, 1, 1);
+    q.dynamicSmemBytes = kd.smem;
+    cudaLaunchAttribute qa;
+    qa.id = cudaLaunchAttributeClusterDimension;
+    qa.val.clusterDim.x = csize;
+    qa.val.clusterDim.y = 1;
+    qa.val.clusterDim.z = 1;
+    q.attrs = &qa;
+    q.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kd.fn, &q) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = st->sms / csize;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    st->max_clusters[idx] = nc;
+  }
+  const int units = kd.mc > 1 ? st->max_clusters[idx] : std::max(1, st->sms / kd.cg);
   // More tiles than co-resident clusters: launch one cluster per tile and let running clusters
   // steal pending ones (cluster launch control) so the tiles in flight stay adjacent in the
   // raster; otherwise every tile gets its own resident cluster.
@@ -356,13 +383,13 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
 
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(clusters * kd.cg, 1, 1);
+  cfg.gridDim = dim3(clusters * csize, 1, 1);
   cfg.blockDim = dim3(kd.threads, 1, 1);
   cfg.dynamicSmemBytes = kd.smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = kd.cg;
+  attrs[0].val.clusterDim.x = csize;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   // Programmatic dependent launch: our prologue may overlap the previous kernel's tail; the
@@ -412,9 +439,9 @@ cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int
   if (id < 0 || id >= kNumGemmCfg) return CY_ERR_INVALID_VALUE;
   const auto& mn = menu();
   for (const auto& k : mn)
-    if (k.var == cy::V_GEMM && k.cg == kGemmMenu[id].cg && k.bn == kGemmMenu[id].bn) {
+    if (k.var == cy::V_GEMM && k.cg == kGemmMenu[id].cg && k.bn == kGemmMenu[id].bn && k.mc == kGemmMenu[id].mc) {
       if (cta_group) *cta_group = k.cg;
-      if (tile_m) *tile_m = 128 * k.cg;
+      if (tile_m) *tile_m = 128 * k.cg * k.mc;
       if (tile_n) *tile_n = k.bn;
       if (stages) *stages = k.stages;
       return CY_OK;
@@ -433,7 +460,7 @@ int cy_last_config(void) {
   if (idx < 0) return -1;
   const auto& k = menu()[idx];
   for (int i = 0; i < kNumGemmCfg; ++i)
-    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn) return i;
+    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn && kGemmMenu[i].mc == k.mc) return i;
   return -1;
 }
 
@@ -446,7 +473,7 @@ cy_status_t cy_last_kernel_info(int* variant, int* cta_group, int* tile_m, int* 
   const KDesc& k = menu()[idx];
   if (variant) *variant = k.var;
   if (cta_group) *cta_group = k.cg;
-  if (tile_m) *tile_m = 128 * k.cg;
+  if (tile_m) *tile_m = 128 * k.cg * k.mc;
   if (tile_n) *tile_n = k.bn;
   if (stages) *stages = k.stages;
   if (threads) *threads = k.threads;

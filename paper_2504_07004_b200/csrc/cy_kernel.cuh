@@ -62,7 +62,7 @@ struct DstMaps {
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1>
+template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1, int MC_ = 1>
 struct Cfg {
   static constexpr int DT = DT_;  // 0 = fp16, 1 = bf16
   static constexpr int CG = CG_;  // CTAs per MMA (tcgen05 cta_group)
@@ -70,6 +70,11 @@ struct Cfg {
   static constexpr int STAGES = STAGES_;
   static constexpr int VAR = VAR_;
   static constexpr int NSUB = NSUB_;          // GEMM: N sub-tiles per tile sharing each A stage
+  // MC = 2: a cluster of two CTA pairs stacked along M shares every B stage: each CTA loads half
+  // of its B atoms and multicasts them to the CTA at the same position in the other pair, so a
+  // 512 x TILE_N cluster tile reads B from L2 once (SURVEY a4 "cluster TMA multicast").
+  static constexpr int MC = MC_;
+  static constexpr int CL = CG * MC;          // cluster size
   static constexpr bool DUAL = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM || VAR == V_DUAL_GLU);
   static constexpr bool GLU = (VAR == V_DUAL_GLU);
   static constexpr int BM_CTA = 128;          // accumulator rows per CTA = TMEM lanes
@@ -114,6 +119,8 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static_assert(NUM_ACC_BUF * ACC_COLS <= 512, "TMEM has 512 columns");
   static_assert(!DUAL || NSUB == 1, "dual GEMM uses its two B slots for B0/B1");
+  static_assert(MC == 1 || (MC == 2 && CG == 2 && VAR == V_GEMM && (NUM_B * BN_CTA / 64) % 2 == 0),
+                "B multicast: GEMM on CTA pairs with an even number of B atoms per stage");
 
   // Instruction descriptor, kind::f16: c_format F32 [4,6) | a_format [7,10) | b_format [10,13) |
   // a_major K (bit 15 = 0) | b_major MN (bit 16 = 1) | N>>3 [17,23) | M>>4 [24,29).
@@ -190,9 +197,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = (C::CG == 2) ? cluster_ctarank() : 0u;
-  const int cid = blockIdx.x / C::CG;
-  const int ncl = gridDim.x / C::CG;
+  const uint32_t crank = (C::CL > 1) ? cluster_ctarank() : 0u;  // rank in the cluster
+  const uint32_t rank = crank & (C::CG - 1);                    // rank in the CTA pair
+  const uint32_t pp = crank / C::CG;                            // pair index in the cluster (MC == 2)
+  const uint32_t leader = crank & ~uint32_t(C::CG - 1);         // this pair's MMA leader
+  const int cid = blockIdx.x / C::CL;
+  const int ncl = gridDim.x / C::CL;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -204,7 +214,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(bFull + 8 * s, 1);
-      mbar_init(bEmpty + 8 * s, 1 + C::RED_WARPS);
+      mbar_init(bEmpty + 8 * s, C::MC + C::RED_WARPS);  // MMA commit of every pair reading it
       if (C::REDUCE) mbar_init(bMDone + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -214,7 +224,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(bCBar + 8 * w, 1);
     for (int j = 0; j < C::SCHED_SLOTS; ++j) {
       mbar_init(bSFull + 8 * j, 1);
-      mbar_init(bSEmpty + 8 * j, C::CG * C::NUM_WARPS);
+      mbar_init(bSEmpty + 8 * j, C::CL * C::NUM_WARPS);
     }
     fence_mbar_init();
   }
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     tmem_relinquish<C::CG>();
   }
   tc_fence_before();
-  if constexpr (C::CG == 2) cluster_sync(); else __syncthreads();
+  if constexpr (C::CL > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Everything above (barrier init, TMEM allocation, descriptor prefetch) overlapped the tail of
@@ -251,10 +261,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     clc_decode(sResp + 16 * j, ok, cx);
     if (warp_wide) __syncwarp();
     if (!warp_wide || lane == 0) {
-      if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bSEmpty + 8 * j, 0));
+      if constexpr (C::CL > 1) mbar_arrive_cluster(mapa(bSEmpty + 8 * j, 0));
       else mbar_arrive(bSEmpty + 8 * j);
     }
-    t = static_cast<int>(cx) / C::CG;
+    t = static_cast<int>(cx) / C::CL;
     return ok != 0;
   };
   // Producer thread, at the start of its tile i: arm this CTA's slot for tile i+1 and (leader)
@@ -263,9 +273,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     if (!p.dyn) return;
     const int j = i % C::SCHED_SLOTS;
     mbar_arrive_expect_tx(bSFull + 8 * j, 16);
-    if (rank == 0) {
+    if (crank == 0) {
       mbar_wait(bSEmpty + 8 * j, ((i / C::SCHED_SLOTS) & 1) ^ 1);
-      if constexpr (C::CG == 2) clc_try_cancel_multicast(sResp + 16 * j, bSFull + 8 * j);
+      if constexpr (C::CL > 1) clc_try_cancel_multicast(sResp + 16 * j, bSFull + 8 * j);
       else clc_try_cancel(sResp + 16 * j, bSFull + 8 * j);
     }
   };
@@ -289,20 +299,20 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         sched_request(i);
         int b, mb, nb;
         tile_coords(p, t, b, mb, nb);
-        const int am = mb * C::BM + rank * C::BM_CTA;
+        const int am = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA;
         const int bn = nb * C::TILE_N + rank * C::BN_CTA;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(bEmpty + 8 * stage, phase ^ 1);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
           if ((p.debug & 1) && (phase || i != 0)) {  // timing experiment: reuse stale stages
-            if (PAIR_TMA ? rank == 0 : true) mbar_arrive(fb);
+            if (PAIR_TMA ? rank == 0 : true) mbar_arrive(fb);  // (MC == 1 only)
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
           if constexpr (PAIR_TMA) {
             if (rank == 0) mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
-            fb = mapa(fb, 0);  // both CTAs count bytes on the leader's barrier
+            fb = mapa(fb, leader);  // both CTAs of the pair count bytes on the leader's barrier
           } else {
             mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
           }
@@ -323,8 +333,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             const CUtensorMap* tmB = (C::DUAL && sl == 1) ? &tmB1 : &tmB0;
             const int cb = bn + (C::DUAL ? 0 : sl * C::BN);
 #pragma unroll
-            for (int j = 0; j < C::BN_CTA / 64; ++j)
-              load(sA + C::A_BYTES + sl * C::B_BYTES + j * C::B_ATOM_BYTES, tmB, cb + 64 * j, k0, pol_b);
+            for (int j = 0; j < C::BN_CTA / 64; ++j) {
+              const uint32_t dst = sA + C::A_BYTES + sl * C::B_BYTES + j * C::B_ATOM_BYTES;
+              if constexpr (C::MC == 2) {
+                // every other atom: ours, multicast to us and our counterpart in the other pair
+                if (((sl * (C::BN_CTA / 64) + j) & 1) == int(pp))
+                  tma_load_3d_pair_mc(dst, tmB, fb, cb + 64 * j, k0, b, uint16_t((1u << crank) | (1u << (crank ^ 2u))),
+                                      pol_b);
+              } else {
+                load(dst, tmB, cb + 64 * j, k0, pol_b);
+              }
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -334,6 +353,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0;
+      constexpr uint16_t kAllMask = uint16_t((1u << C::CL) - 1u);  // stage release: every CTA of the cluster
+      const uint16_t pair_mask = uint16_t(0x3u << leader);          // this pair's two CTAs
       // all 4 k16 MMAs of one k-block for B slot `sl` of ring stage `st` into accumulator base `d`
       auto issue = [&](uint32_t d, int st, int sl, int kb) {
         const uint32_t sA = sStage0 + st * C::STAGE_BYTES;
@@ -371,8 +392,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       };
       auto release = [&](int st) {
-        mma_commit<C::CG>(bEmpty + 8 * st, 0x3);  // frees the stage in both CTAs
-        if constexpr (C::REDUCE) mma_commit<C::CG>(bMDone + 8 * st, 0x3);  // reducers may read it
+        mma_commit<C::CG>(bEmpty + 8 * st, kAllMask);  // frees the stage (B multicast: in both pairs)
+        if constexpr (C::REDUCE) mma_commit<C::CG>(bMDone + 8 * st, pair_mask);  // reducers may read it
       };
       int t;
       for (int it = 0; sched_next(it, t, false); ++it) {
@@ -440,7 +461,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             flush();
           }
         }
-        mma_commit<C::CG>(bTFull + 8 * buf, 0x3);      // accumulator ready, both CTAs
+        mma_commit<C::CG>(bTFull + 8 * buf, pair_mask);  // accumulator ready, both CTAs of the pair
       }
     } else if (lane == 0) {
       // peer CTA: the leader issues all MMAs; follow the tile schedule only
@@ -466,14 +487,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
       else mbar_wait(bTFull + 8 * buf, bph);
       tc_fence_after();
-      const int row0 = mb * C::BM + rank * C::BM_CTA + 32 * q;
+      const int row0 = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA + 32 * q;
       if (p.debug & 2) {  // timing experiment: drop the epilogue
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           for (int a = 0; a < (C::SPLIT ? 2 : 1); ++a) {
             const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
-            if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, 0));
+            if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, leader));
             else mbar_arrive(bar);
           }
         }
@@ -524,7 +545,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             __syncwarp();
             if (lane == 0) {
               const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
-              if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, 0));
+              if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, leader));
               else mbar_arrive(bar);
             }
           }
@@ -611,7 +632,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 
   __syncwarp();
   tc_fence_before();
-  if constexpr (C::CG == 2) cluster_sync(); else __syncthreads();
+  if constexpr (C::CL > 1) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::CG>(tmem_base, C::TMEM_COLS);

@@ -142,6 +142,17 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// CTA-pair form with multicast: the box lands at offset `dst` in every CTA of `cta_mask`; each
+// destination's completion bytes are counted on the barrier at `bar_cluster`'s offset in that
+// destination's pair leader (cta_group::2 semantics; callers pass their own pair leader's barrier).
+__device__ __forceinline__ void tma_load_3d_pair_mc(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster,
+                                                    int c0, int c1, int c2, uint16_t cta_mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_nohint(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0,
                                                    int c1, int c2) {
   asm volatile(
