@@ -378,7 +378,8 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   // More tiles than co-resident clusters: launch one cluster per tile and let running clusters
   // steal pending ones (cluster launch control) so the tiles in flight stay adjacent in the
   // raster; otherwise every tile gets its own resident cluster.
-  p.dyn = (p.tiles > units && g_sched != 1) ? 1 : 0;
+  // CY_SCHED=2: one cluster per tile and no stealing (the non-persistent launch) -- tuning knob
+  p.dyn = (p.tiles > units && g_sched != 1) ? (g_sched == 2 ? 2 : 1) : 0;
   const int clusters = p.dyn ? p.tiles : std::max(1, std::min(p.tiles, units));
 
   cudaLaunchConfig_t cfg;

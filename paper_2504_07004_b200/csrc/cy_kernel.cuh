@@ -50,7 +50,8 @@ struct Params {
   int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
   int sleep_ns;          // >0: epilogue waits for the accumulator with nanosleep backoff (cap, ns)
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
-                         //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride
+                         //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride;
+                         // 2: one cluster per tile, no stealing (non-persistent)
 };
 
 // Extra destinations of every D tile (fused replication): tensor maps over this
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       t = cid;
       return t < p.tiles;
     }
+    if (p.dyn == 2) return false;  // one tile per launched cluster, no stealing
     const int j = (i - 1) % C::SCHED_SLOTS;
     const uint32_t ph = ((i - 1) / C::SCHED_SLOTS) & 1;
     mbar_wait(bSFull + 8 * j, ph);
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   // Producer thread, at the start of its tile i: arm this CTA's slot for tile i+1 and (leader)
   // ask the hardware for the next pending cluster.
   auto sched_request = [&](int i) {
-    if (!p.dyn) return;
+    if (p.dyn != 1) return;
     const int j = i % C::SCHED_SLOTS;
     mbar_arrive_expect_tx(bSFull + 8 * j, 16);
     if (crank == 0) {
