@@ -311,6 +311,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nk; ++j) {
       mbar_wait(bSFull + 8 * t, j & 1);
+      // PV_t(j-1) was issued before S_t(j) and tcgen05 ops complete in order, so this never blocks;
+      // consuming every phase keeps the barrier protocol explicit (and compute-sanitizer clean)
+      if (j > 0) mbar_wait(bOReady + 8 * t, (j - 1) & 1);
       tc_fence_after();
       const int key0 = j * BKV;
       const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= trow0);
@@ -352,9 +355,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         corr = ex2(m - m_new);  // 0 when m == -inf
       }
       const float msub = (m_new == -INFINITY) ? 0.f : m_new;
-      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
-        mbar_wait(bOReady + 8 * t, (j - 1) & 1);  // O_t holds PV_t(j-1)
-        tc_fence_after();
+      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O_t holds PV_t(j-1) (waited above)
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
