@@ -61,6 +61,7 @@ struct Params {
   int causal;
   float scale_log2;  // scale * log2(e)
   float* lse;        // [bh, sq] natural-log lse, or null
+  int l2hint;        // 1: TMA loads carry an L2 evict_last hint; 0: no hint (requests can merge in L2)
 };
 
 template <int DT, bool B_MN>
@@ -228,22 +229,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- producer
     if (lane == 0 && nall > 0) {
       const uint64_t pol = policy_evict_last();
+      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1) {
+        if (p.l2hint) tma_load_3d(dst, tm, bar, c0, c1, hb, pol);
+        else tma_load_3d_nohint(dst, tm, bar, c0, c1, hb);
+      };
       mbar_arrive_expect_tx(bQFull, NT * TILE);
       for (int t = 0; t < NT; ++t) {
-        tma_load_3d(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t, hb, pol);
-        tma_load_3d(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, q0 + BQ * t, hb, pol);
+        ld(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t);
+        ld(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, q0 + BQ * t);
       }
       for (int j = 0; j < nall; ++j) {
         const int s = j & 1;
         const int k0 = j * BKV;
         mbar_wait(bKEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(bKFull + 8 * s, TILE);
-        tma_load_3d(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0, hb, pol);
-        tma_load_3d(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0, hb, pol);
+        ld(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0);
+        ld(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0);
         mbar_wait(bVEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(bVFull + 8 * s, TILE);
-        tma_load_3d(sV + s * TILE, &tmV, bVFull + 8 * s, 0, k0, hb, pol);
-        tma_load_3d(sV + s * TILE + ATOM, &tmV, bVFull + 8 * s, 64, k0, hb, pol);
+        ld(sV + s * TILE, &tmV, bVFull + 8 * s, 0, k0);
+        ld(sV + s * TILE + ATOM, &tmV, bVFull + 8 * s, 64, k0);
       }
     }
   } else if (warp == W_MMA) {
@@ -581,19 +586,23 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
       const uint64_t pol = policy_evict_last();
       if (rank == 0) mbar_arrive_expect_tx(bQFull, 2 * Q_BYTES);
       const uint32_t qb = mapa(bQFull, 0);
-      tma_load_3d_pair(sQ, &tmQ, qb, 0, trow0, hb, pol);
-      tma_load_3d_pair(sQ + QATOM, &tmQ, qb, 64, trow0, hb, pol);
+      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1) {
+        if (p.l2hint) tma_load_3d_pair(dst, tm, bar, c0, c1, hb, pol);
+        else tma_load_3d_pair_nohint(dst, tm, bar, c0, c1, hb);
+      };
+      ld(sQ, &tmQ, qb, 0, trow0);
+      ld(sQ + QATOM, &tmQ, qb, 64, trow0);
       for (int j = 0; j < n; ++j) {
         const int ks = j % KS, vs = j % VS;
         mbar_wait(bKEmpty + 8 * ks, ((j / KS) & 1) ^ 1);
         if (rank == 0) mbar_arrive_expect_tx(bKFull + 8 * ks, 2 * K_BYTES);
         const uint32_t kb = mapa(bKFull + 8 * ks, 0);
         const int key0 = j * BKV + 64 * int(rank);
-        tma_load_3d_pair(sK + ks * K_BYTES, &tmK, kb, 0, key0, hb, pol);
-        tma_load_3d_pair(sK + ks * K_BYTES + KATOM, &tmK, kb, 64, key0, hb, pol);
+        ld(sK + ks * K_BYTES, &tmK, kb, 0, key0);
+        ld(sK + ks * K_BYTES + KATOM, &tmK, kb, 64, key0);
         mbar_wait(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
         if (rank == 0) mbar_arrive_expect_tx(bVFull + 8 * vs, 2 * V_BYTES);
-        tma_load_3d_pair(sV + vs * V_BYTES, &tmV, mapa(bVFull + 8 * vs, 0), 64 * int(rank), j * BKV, hb, pol);
+        ld(sV + vs * V_BYTES, &tmV, mapa(bVFull + 8 * vs, 0), 64 * int(rank), j * BKV);
       }
     }
   } else if (warp == W_MMA) {
@@ -880,6 +889,11 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.lse = lse;
+  // CY_ATTN_L2HINT: 1 = evict_last hint on the Q/K/V TMA loads, 0 = none (tuning knob)
+  p.l2hint = [] {
+    const char* e = std::getenv("CY_ATTN_L2HINT");
+    return e ? std::atoi(e) : 1;
+  }();
   // CY_ATTN_EMU: how many of every 8 exponential pairs run on the FMA pipe (tuning knob; default 0).
   // Measured on B200 (scripts/mufu_probe.cu): MUFU.EX2 16/clk/SM, FFMA2 ~56 pairs/clk/SM (half
   // rate), so a cubic exp2 costs about as much FMA-pipe time as MUFU time: at most +12% on the
