@@ -402,6 +402,19 @@ def test_dual_glu_integer_and_large():
     assert (np.abs(decode(D[rows], "f16") - ref) <= tol).all()
 
 
+def test_dual_pair_8192_sampled():
+    """BASELINE configs[3]: D = (A*B0, A*B1) at 8192^3 (the bench workload and launch), oracle on
+    sampled rows of both outputs."""
+    n = 8192
+    A, B0, B1, _, _ = synth.dual_inputs(n, n, n, seed=synth.seed_for(3, 0))
+    d0, d1 = cy.dual_gemm(to_dev(A, "f16"), to_dev(B0, "f16"), to_dev(B1, "f16"), mode="pair")
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(n, n_random=8)[::3]
+    r0, r1 = oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows)
+    assert_within_tol(to_bits(d0)[rows], r0, n, "f16", what="D0 8192^3 sampled")
+    assert_within_tol(to_bits(d1)[rows], r1, n, "f16", what="D1 8192^3 sampled")
+
+
 # ---------------------------------------------------------------- fused replication (NEXT-2)
 @pytest.mark.parametrize("ndst", [1, 3, 8])
 @pytest.mark.parametrize("cfg", [-1, 0, 3])
@@ -623,6 +636,33 @@ def test_attention_counts_one_launch():
     cy.attention(*(to_dev(x, "f16").view(1, 2, 256, 128) for x in (Q, K, V)))
     torch.cuda.synchronize()
     assert cy.launch_count() - n0 == 1
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_bench_shape_sampled(causal):
+    """The attention bench workload exactly (2 x 16 heads x 8192, HeadDim 128, the same seeded
+    inputs and call), oracle on sampled query rows of every head, O and lse."""
+    b, h, s, d = 2, 16, 8192, 128
+    Q, K, V = (synth.uniform((b * h, s, d), synth.seed_for(6, t)) for t in range(3))
+    O, lse = cy.attention(*(to_dev(x, "f16").view(b, h, s, d) for x in (Q, K, V)), causal=causal)
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(s, n_random=4)[::6]
+    if causal:  # the oracle evaluates query rows as positions 0..len(rows)-1: test row r against keys <= r
+        Kr = [K[:, : r + 1] for r in rows]
+    Oref = np.empty((b * h, len(rows), d))
+    lref = np.empty((b * h, len(rows)))
+    if not causal:
+        Oref, lref = oracle.attention("f16", np.ascontiguousarray(Q[:, rows]), K, V)
+    else:
+        for i, r in enumerate(rows):
+            o, l = oracle.attention("f16", np.ascontiguousarray(Q[:, r:r + 1]), Kr[i], np.ascontiguousarray(V[:, : r + 1]))
+            Oref[:, i] = o[:, 0]
+            lref[:, i] = l[:, 0]
+    got = decode(to_bits(O).reshape(b * h, s, d)[:, rows], "f16")
+    u = 2.0 ** -11
+    tol = 2 * u * np.abs(decode(V, "f16")).max() + 3 * u * np.abs(Oref) + 1e-6
+    assert (np.abs(got - Oref) <= tol).all(), f"max err/tol {(np.abs(got - Oref) / tol).max():.3f}"
+    assert np.allclose(lse.reshape(b * h, s)[:, rows].cpu().numpy(), lref, rtol=0, atol=2e-3 + 4 * u)
 
 
 def test_attention_large_sampled():
