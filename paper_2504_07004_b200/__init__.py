@@ -68,36 +68,39 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
-def _stream(stream, like=None):
+def _stream(stream, dev):
     if stream is None:
         torch = _torch()
-        dev = like.device.index if like is not None and like.device.index is not None else torch.cuda.current_device()
-        return torch._C._cuda_getCurrentRawStream(dev)
+        return torch._C._cuda_getCurrentRawStream(dev if dev >= 0 else torch.cuda.current_device())
     return getattr(stream, "cuda_stream", stream)
 
 
 def _check_dev(*ts):
-    dev = None
+    """All tensors must live on one CUDA device, which becomes the current device (the C ABI works
+    on the current device, torch semantics).  Returns the device index.  Uses get_device() (an int)
+    rather than .device objects: this runs on every call."""
+    dev = -2
     for t in ts:
         if t is None:
             continue
-        if not t.is_cuda:
+        g = t.get_device()
+        if g < 0:
             raise ValueError("cypress_b200: all tensors must be CUDA tensors (no CPU fallback)")
-        if dev is None:
-            dev = t.device
-        elif t.device != dev:
-            raise ValueError(f"cypress_b200: tensors on different devices ({dev} vs {t.device})")
-    if dev is not None and dev.index is not None:
+        if dev == -2:
+            dev = g
+        elif g != dev:
+            raise ValueError(f"cypress_b200: tensors on different devices (cuda:{dev} vs cuda:{g})")
+    if dev >= 0:
         torch = _torch()
-        if torch.cuda.current_device() != dev.index:
-            # the C ABI works on the current device: follow the tensors (torch semantics)
-            torch.cuda.set_device(dev.index)
+        if torch.cuda.current_device() != dev:
+            torch.cuda.set_device(dev)
+    return dev
 
 
 def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
     """D = alpha*A@B + beta*C  (A: m x k, B: k x n, row-major).  cy_gemm."""
     torch = _torch()
-    _check_dev(A, B, C, out)
+    dev = _check_dev(A, B, C, out)
     m, k = A.shape
     n = B.shape[1]
     if B.shape[0] != k:
@@ -107,7 +110,7 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=N
     lib = _lib.load()
     st = lib.cy_gemm(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
                      _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n,
-                     _ptr(out), _ld(out, "out"), _stream(stream, A))
+                     _ptr(out), _ld(out, "out"), _stream(stream, dev))
     check(st, "cy_gemm")
     return out
 
@@ -115,7 +118,7 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=N
 def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
     """D[b] = alpha*A[b]@B[b] + beta*C[b] for b < L (3-D tensors, rows contiguous)."""
     torch = _torch()
-    _check_dev(A, B, C, out)
+    dev = _check_dev(A, B, C, out)
     L, m, k = A.shape
     n = B.shape[2]
     if out is None:
@@ -134,7 +137,7 @@ def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, 
     ldd, sd = lds(out)
     st = _lib.load().cy_gemm_batched(_dt(A), m, n, k, L, float(alpha), _ptr(A), lda, sa, _ptr(B), ldb, sb,
                                      float(beta), _ptr(C) if beta != 0 else None, ldc, sc, _ptr(out), ldd, sd,
-                                     _stream(stream, A))
+                                     _stream(stream, dev))
     check(st, "cy_gemm_batched")
     return out
 
@@ -144,7 +147,7 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
     """mode "pair": (D0, D1) = (alpha*A@B0 + beta*C0, alpha*A@B1 + beta*C1);
     mode "sum": D = alpha*(A@B0 + A@B1) + beta*C0.  cy_dual_gemm."""
     torch = _torch()
-    _check_dev(A, B0, B1, C0, C1, out0, out1)
+    dev = _check_dev(A, B0, B1, C0, C1, out0, out1)
     m, k = A.shape
     n = B0.shape[1]
     pair = mode == "pair"
@@ -160,7 +163,7 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
         _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), float(beta), _ptr(C0) if use_c else None,
         _ld(C0, "C0") if (use_c and C0 is not None) else n, _ptr(C1) if (use_c and pair) else None,
         _ld(C1, "C1") if (use_c and pair and C1 is not None) else n, _ptr(out0), _ld(out0, "out0"),
-        _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, A))
+        _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, dev))
     check(st, "cy_dual_gemm")
     return (out0, out1) if pair else out0
 
@@ -170,7 +173,7 @@ def attention(Q, K, V, scale=None, causal: bool = False, out=None, lse=None, str
     Q: (batch, heads, seq_q, 128), K/V: (batch, heads, seq_k, 128), contiguous fp16/bf16.
     Returns (O, lse) with lse (batch, heads, seq_q) fp32 natural log-sum-exp.  cy_attention_fwd."""
     torch = _torch()
-    _check_dev(Q, K, V, out, lse)
+    dev = _check_dev(Q, K, V, out, lse)
     b, h, sq, d = Q.shape
     sk = K.shape[2]
     for t, name in ((Q, "Q"), (K, "K"), (V, "V")):
@@ -183,7 +186,7 @@ def attention(Q, K, V, scale=None, causal: bool = False, out=None, lse=None, str
     if lse is None:
         lse = torch.empty((b, h, sq), dtype=torch.float32, device=Q.device)
     st = _lib.load().cy_attention_fwd(_dt(Q), b, h, sq, sk, d, float(scale), int(bool(causal)), _ptr(Q), _ptr(K),
-                                      _ptr(V), _ptr(out), _ptr(lse), _stream(stream, Q))
+                                      _ptr(V), _ptr(out), _ptr(lse), _stream(stream, dev))
     check(st, "cy_attention_fwd")
     return out, lse
 
@@ -195,7 +198,7 @@ def gemm_replicated(A, B, dsts, row_offset: int, rows_total: int, C=None, alpha:
     cy_gemm_replicated (fused replication; the destinations are usually peers' buffers)."""
     import ctypes
 
-    _check_dev(A, B, C)
+    dev = _check_dev(A, B, C)
     m, k = A.shape
     n = B.shape[1]
     ptrs = [d if isinstance(d, int) else d.data_ptr() for d in dsts]
@@ -204,13 +207,13 @@ def gemm_replicated(A, B, dsts, row_offset: int, rows_total: int, C=None, alpha:
     st = _lib.load().cy_gemm_replicated(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"),
                                         float(beta), _ptr(C) if beta != 0 else None,
                                         _ld(C, "C") if (C is not None and beta != 0) else n, arr, len(ptrs), ldd,
-                                        int(row_offset), int(rows_total), _stream(stream, A))
+                                        int(row_offset), int(rows_total), _stream(stream, dev))
     check(st, "cy_gemm_replicated")
 
 
 def dual_gemm_glu(A, B0, B1, act: str = "silu", alpha: float = 1.0, out=None, stream=None):
     """D = act(alpha*A@B0) * (alpha*A@B1), act in {"silu", "gelu_tanh"} (GLU).  cy_dual_gemm_glu."""
-    _check_dev(A, B0, B1, out)
+    dev = _check_dev(A, B0, B1, out)
     m, k = A.shape
     n = B0.shape[1]
     a = {"silu": _lib.CY_ACT_SILU, "gelu_tanh": _lib.CY_ACT_GELU_TANH}[act]
@@ -218,7 +221,7 @@ def dual_gemm_glu(A, B0, B1, act: str = "silu", alpha: float = 1.0, out=None, st
         out = _empty2d(m, n, A)
     st = _lib.load().cy_dual_gemm_glu(_dt(A), a, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
                                       _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), _ptr(out), _ld(out, "out"),
-                                      _stream(stream, A))
+                                      _stream(stream, dev))
     check(st, "cy_dual_gemm_glu")
     return out
 
@@ -226,7 +229,7 @@ def dual_gemm_glu(A, B0, B1, act: str = "silu", alpha: float = 1.0, out=None, st
 def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, y=None, stream=None):
     """D = alpha*A@B + beta*C and y[i] = sum_k A[i,k] (fp32), one kernel.  cy_gemm_rowreduce."""
     torch = _torch()
-    _check_dev(A, B, C, out, y)
+    dev = _check_dev(A, B, C, out, y)
     m, k = A.shape
     n = B.shape[1]
     if out is None:
@@ -236,7 +239,7 @@ def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None
     st = _lib.load().cy_gemm_rowreduce(
         _dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
         _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n, _ptr(out),
-        _ld(out, "out"), _ptr(y), _stream(stream, A))
+        _ld(out, "out"), _ptr(y), _stream(stream, dev))
     check(st, "cy_gemm_rowreduce")
     return out, y
 
