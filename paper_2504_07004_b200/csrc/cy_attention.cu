@@ -3,21 +3,21 @@
 //
 //   S = scale * Q K^T,  P = softmax_rows(S) (causal: key j <= query i),  O = P V,  lse = log sum exp S
 //
-// One CTA per (two 128-row query tiles, batch*head).  Warp roles:
-//   warp 0      TMA producer: Q tile once, then K_j / V_j blocks (128 keys) into a 2-stage ring.
-//   warp 1      tcgen05.mma issuer: S_j = Q K_j^T into one of two TMEM score buffers, then
-//               O += P_j V_j into the TMEM output accumulator.  It issues S_{j+1} before waiting for
-//               P_j, so the tensor core computes the next scores while the SIMT warps run the
-//               softmax of block j -- the FA3 software pipeline expressed with two
-//               TMEM score buffers instead of a register copy.
-//   warps 2-5,  softmax warpgroups for query tiles 0 and 1 (thread = query row = TMEM lane):
-//   warps 6-9   S_t read once from TMEM into registers, running row max / sum in the exp2 domain,
-//               P_t (16-bit) written back over S_t in TMEM and consumed by tcgen05.mma with A from
-//               TMEM, lazy rescale of the O_t accumulator (only when the row max grows by > 2^8),
-//               final O / l normalisation + TMA store and lse.  While one warpgroup runs its softmax
-//               the tensor core computes the other tile's S and P.V (ping-pong), and every K/V
-//               block is reused by both tiles.
-// TMEM: S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512).  Shared: Q 2 x 32 KB, K/V 2 x 64 KB.
+// attn_fwd_kernel (default): one CTA per (two 128-row query tiles, batch*head), 10 warps.
+//   warps 0-3, 4-7  softmax warpgroups of query tiles 0 and 1 (thread = query row = TMEM lane): per
+//                   128-key block, pass 1 reads S_t from TMEM for the row max, pass 2 re-reads it,
+//                   computes P = exp2(s*scale*log2e - m) in the exp2 domain and writes P_t (16-bit
+//                   pairs) back over S_t; lazy rescale of O_t in TMEM only when the max grows by
+//                   more than 2^8; final O / l, TMA store, lse.
+//   warp 8          TMA producer: both Q tiles once, then K_j and V_j through two separate 2-slot
+//                   rings (each refilled as soon as its last reader is done).
+//   warp 9          tcgen05.mma issuer, per block j and tile t: O_t += P_t V_j (A = P_t read from
+//                   TMEM), then S_t(j+1) = Q_t K_{j+1}^T.  While one warpgroup runs its softmax the
+//                   tensor core runs the other tile's two GEMMs -- the FA3 ping-pong
+//                   with TMEM in place of FA3's register copy of S; every K/V block serves 256 rows.
+//   TMEM: S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512).  Shared: Q 2 x 32 KB, K/V 2 x 64 KB.
+// attn_pair_kernel (CY_ATTN_KERNEL=2): a CTA pair issuing cta_group::2 MMAs with double-buffered
+//   S and a separate P in TMEM (see its own comment); correct, measured slower.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
