@@ -51,7 +51,8 @@ constexpr int SQ_OFF = 0;                  // [NT]
 constexpr int SK_OFF = NT * TILE;          // [2]
 constexpr int SV_OFF = (NT + 2) * TILE;    // [2]
 constexpr int BAR_OFF = (NT + 4) * TILE;
-constexpr int SMEM_BYTES = 1024 + (NT + 4) * TILE + 256;
+constexpr int XCH_OFF = BAR_OFF + 256;       // CS = 2: row-max exchange [NT][2][2][BQ], sums [NT][2][BQ]
+constexpr int SMEM_BYTES = 1024 + (NT + 4) * TILE + 256 + (NT * 2 * 2 * BQ + NT * 2 * BQ) * 4;
 constexpr int THREADS = (4 * NT + 2) * 32;  // softmax warpgroups 0..NT-1, then producer, MMA issuer
 constexpr int W_PROD = 4 * NT, W_MMA = 4 * NT + 1;
 constexpr uint32_t TM_S = 0, TM_O = 256;   // S_t at 128 t, O_t at 256 + 128 t
@@ -170,7 +171,10 @@ __device__ __forceinline__ int blocks_for(const Params& p, int row_end) {
   return (kv_end + BKV - 1) / BKV;
 }
 
-template <int DT, int EMU>  // EMU of every 8 exponential pairs are evaluated with ex2_emu2
+// EMU of every 8 exponential pairs are evaluated with ex2_emu2.  CS = 1: warpgroup t owns query
+// tile t (one warp per row quarter); CS = 2: all 8 softmax warps work on each tile in turn, the
+// two warps of a row quarter splitting its 128 scores (two warps per SM sub-partition per tile).
+template <int DT, int EMU, int CS = 1>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -187,6 +191,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // P_t columns inside S_t: CS = 1 writes P over columns [0, 64); CS = 2 over [32, 96), so each
+  // half-row warp overwrites only score columns it has already read itself
+  constexpr uint32_t P_COL = (CS == 2) ? 32 : 0;
   const int qt = p.causal ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;  // heavy causal CTAs first
   const int hb = blockIdx.y;
   const int q0 = qt * BQ * NT;
@@ -209,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int t = 0; t < NT; ++t) {
       mbar_init(bSFull + 8 * t, 1);
-      mbar_init(bPReady + 8 * t, 4);
+      mbar_init(bPReady + 8 * t, 4 * CS);
       mbar_init(bOReady + 8 * t, 1);
     }
     fence_mbar_init();
@@ -275,8 +282,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // S_t(j+1) is issued after this and tcgen05 ops execute in order, so it cannot clobber P_t.
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + kk * 8, sdesc_sw128(v + kk * 2048, ATOM, 1024),
-                     ID_PV, (j | kk) != 0);
+          mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8,
+                     sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV, (j | kk) != 0);
         mma_commit<1>(bOReady + 8 * t, 0);
       };
       mbar_wait(bQFull, 0);
@@ -302,6 +309,155 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (next) mma_commit<1>(bKEmpty + 8 * ((j + 1) & 1), 0);  // K_{j+1} consumed
       }
     }
+  } else if constexpr (CS == 2) {
+    // ---------------------------------------------------------------- softmax, both tiles, split rows
+    const int h = warp >> 2;        // column half: scores [64h, 64h+64), O columns [64h, 64h+64)
+    const int q = warp & 3;         // TMEM lane quarter
+    const int r = 32 * q + lane;
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    float* xmax = reinterpret_cast<float*>(smem_raw + (base + XCH_OFF - raw));  // [NT][2 parity][2][BQ]
+    float* xl = xmax + NT * 2 * 2 * BQ;                                         // [NT][2][BQ]
+    const uint32_t bar_id = 1 + q;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    float m[NT], l[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      m[t] = -INFINITY;
+      l[t] = 0.f;
+    }
+    for (int j = 0; j < nall; ++j) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (j >= nkv[t]) continue;
+        const int trow0 = q0 + BQ * t;
+        const int qrow = trow0 + r;
+        const uint32_t tS = tmem + lane_base + TM_S + t * 128;
+        const uint32_t tO = tmem + lane_base + TM_O + t * 128 + 64 * h;
+        mbar_wait(bSFull + 8 * t, j & 1);
+        if (j > 0) mbar_wait(bOReady + 8 * t, (j - 1) & 1);  // never blocks (see CS = 1)
+        tc_fence_after();
+        uint32_t v[64];
+        tmem_ld_32x32b_x32(tS + 64 * h, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        tmem_ld_32x32b_x32(tS + 64 * h + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        tmem_ld_wait();
+        const int key0 = j * BKV + 64 * h;
+        const bool full_block = (j * BKV + BKV <= p.sk) && (!p.causal || j * BKV + BKV - 1 <= trow0);
+        if (!full_block) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            const int key = key0 + e;
+            if (key >= p.sk || (p.causal && key > qrow)) v[e] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+        const float mh = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        float* xm = xmax + ((t * 2 + (j & 1)) * 2) * BQ;
+        xm[h * BQ + r] = mh;
+        pair_sync();  // (also: both halves have read S_t(j) before either half's P store)
+        float mb = fmaxf(xm[r], xm[BQ + r]);
+        mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;
+        float m_new = m[t], corr = 1.f;
+        if (mb > m[t] + 8.f) {
+          m_new = mb;
+          corr = ex2(m[t] - m_new);
+        }
+        const float msub = (m_new == -INFINITY) ? 0.f : m_new;
+        if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O_t holds PV_t(j-1)
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x32(tO + 32 * c, o);
+          }
+        }
+        float2 sm4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 ms2 = make_float2(-msub, -msub);
+        uint32_t pk[32];
+        auto exps = [&](auto e_c) {
+          constexpr int E = decltype(e_c)::value;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float2 x = ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sc2, ms2);
+            float2 pe;
+            if ((e & 7) < E) {
+              pe = ex2_emu2(x);
+            } else {
+              pe.x = ex2(x.x);
+              pe.y = ex2(x.y);
+            }
+            sm4[e & 3] = fadd2(sm4[e & 3], pe);
+            pk[e] = pack2<DT>(pe.x, pe.y);
+          }
+        };
+        if (EMU > 0 && full_block)
+          exps(std::integral_constant<int, EMU>{});
+        else
+          exps(std::integral_constant<int, 0>{});
+        // keys [64h, 64h+64) -> P columns P_COL + [32h, 32h+32) = score columns of this half only
+        tmem_st_32x32b_x32(tS + P_COL + 32 * h, pk);
+        tmem_st_wait();
+        l[t] = l[t] * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
+                              ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
+        m[t] = m_new;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bPReady + 8 * t);
+      }
+    }
+    // ---------------------------------------------------------------- epilogue: both tiles
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int nk = nkv[t];
+      const int trow0 = q0 + BQ * t;
+      const int qrow = trow0 + r;
+      const uint32_t tO = tmem + lane_base + TM_O + t * 128 + 64 * h;
+      xl[(t * 2 + h) * BQ + r] = l[t];
+      pair_sync();
+      const float lt = xl[(t * 2) * BQ + r] + xl[(t * 2 + 1) * BQ + r];
+      const float inv_l = (lt > 0.f) ? 1.f / lt : 0.f;
+      if (nk > 0) {
+        mbar_wait(bOReady + 8 * t, (nk - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t sE = sQ + t * TILE + (h * 4 + q) * 4096;  // Q_t is no longer read: 4 KB per warp
+      uint32_t a[64];
+      if (nk > 0) {
+        tmem_ld_32x32b_x32(tO, *reinterpret_cast<uint32_t(*)[32]>(&a[0]));
+        tmem_ld_32x32b_x32(tO + 32, *reinterpret_cast<uint32_t(*)[32]>(&a[32]));
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) a[e] = 0u;
+      }
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv) {
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          w[u] = pack2<DT>(__uint_as_float(a[8 * vv + 2 * u]) * inv_l, __uint_as_float(a[8 * vv + 2 * u + 1]) * inv_l);
+        st_shared_v4(sE + lane * 128 + ((vv ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&tmO, sE, 64 * h, trow0 + 32 * q, hb);
+        bulk_commit();
+      }
+      if (h == 0 && p.lse && qrow < p.sq)
+        p.lse[(size_t)hb * p.sq + qrow] = (lt > 0.f) ? (m[t] + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
+    }
+    if (lane == 0) bulk_wait_read<0>();
   } else if (warp < 4 * NT) {
     // ---------------------------------------------------------------- softmax / correction / epilogue
     const int t = warp >> 2;        // query tile of this warpgroup
@@ -988,7 +1144,7 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_attr_mu;
-bool g_attr_set[64][4][2][4] = {};
+bool g_attr_set[64][5][2][4] = {};
 
 bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r,
               bool swizzle = true) {
@@ -1082,7 +1238,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     const int v = e ? std::atoi(e) : 0;
     return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 0;
   }();
-  const void* fns[4][2][4] = {
+  const void* fns[5][2][4] = {
       {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
         (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
        {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
@@ -1098,9 +1254,18 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
       {{(const void*)&attn_pair_kernel<0, 0, 1>, (const void*)&attn_pair_kernel<0, 2, 1>,
         (const void*)&attn_pair_kernel<0, 3, 1>, (const void*)&attn_pair_kernel<0, 4, 1>},
        {(const void*)&attn_pair_kernel<1, 0, 1>, (const void*)&attn_pair_kernel<1, 2, 1>,
-        (const void*)&attn_pair_kernel<1, 3, 1>, (const void*)&attn_pair_kernel<1, 4, 1>}}};
+        (const void*)&attn_pair_kernel<1, 3, 1>, (const void*)&attn_pair_kernel<1, 4, 1>}},
+      {{(const void*)&attn_fwd_kernel<0, 0, 2>, (const void*)&attn_fwd_kernel<0, 2, 2>,
+        (const void*)&attn_fwd_kernel<0, 3, 2>, (const void*)&attn_fwd_kernel<0, 4, 2>},
+       {(const void*)&attn_fwd_kernel<1, 0, 2>, (const void*)&attn_fwd_kernel<1, 2, 2>,
+        (const void*)&attn_fwd_kernel<1, 3, 2>, (const void*)&attn_fwd_kernel<1, 4, 2>}}};
   const int ei = emu == 0 ? 0 : emu - 1;
-  const int ki = kern == 1 ? 0 : (split == 2 ? 1 : split == 4 ? 2 : 3);
+  // CY_ATTN_CS: two-tile kernel row split, 1 (one warp per row) or 2 (two warps per row, both tiles)
+  const int cs = [] {
+    const char* e = std::getenv("CY_ATTN_CS");
+    return (e && std::atoi(e) == 2) ? 2 : 1;
+  }();
+  const int ki = kern == 1 ? (cs == 2 ? 4 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
   const void* fn = fns[ki][dt][ei];
   const int smem = kern == 2 ? pr::SMEM_BYTES : SMEM_BYTES;
   {
