@@ -76,6 +76,21 @@ __global__ void k(uint32_t* out, int iters, float seed) {
         v[2 * i] = x.x;
         v[2 * i + 1] = x.y;
       }
+    } else if (OP == 10) {  // the step with PRMT (truncating) packing instead of F2FP
+      const float2 sc = make_float2(0.0901f, 0.0901f), ms = make_float2(-seed, -seed);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float2 x = ffma2(make_float2(v[2 * i], v[2 * i + 1]), sc, ms);
+        float2 p;
+        p.x = ex2(x.x);
+        p.y = ex2(x.y);
+        sm[i & 3] = fadd2(sm[i & 3], p);
+        uint32_t u;
+        asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(u) : "r"(__float_as_uint(p.x)), "r"(__float_as_uint(p.y)));
+        acc ^= u;
+      }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(__float_as_uint(v[i]) ^ (acc & 1));
     } else if (OP == 8) {  // ex2.approx.f16x2: two exponentials per instruction
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -117,10 +132,11 @@ int main() {
   cudaEventCreate(&e1);
   int clk;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  const char* names[9] = {"ex2 (elem)", "f2fp pack (pair)", "ffma2 (pair)", "softmax step (elem)",
+  const char* names[11] = {"ex2 (elem)", "f2fp pack (pair)", "ffma2 (pair)", "softmax step (elem)",
                           "step emu 1/8 (elem)", "step emu 2/8 (elem)", "step emu 3/8 (elem)", "step emu 4/8 (elem)",
-                          "ex2.f16x2 (pair)"};
-  for (int op = 0; op < 9; ++op)
+                          "ex2.f16x2 (pair)", "", "step, prmt pack (elem)"};
+  for (int op = 0; op < 11; ++op) {
+    if (op == 9) continue;
     for (int th : {128, 256, 512}) {
       const int iters = 512;
       float ms = 0;
@@ -134,14 +150,16 @@ int main() {
         else if (op == 5) k<5><<<148, th>>>(o, iters, 1e-3f);
         else if (op == 6) k<6><<<148, th>>>(o, iters, 1e-3f);
         else if (op == 7) k<7><<<148, th>>>(o, iters, 1e-3f);
-        else k<8><<<148, th>>>(o, iters, 1e-3f);
+        else if (op == 8) k<8><<<148, th>>>(o, iters, 1e-3f);
+        else k<10><<<148, th>>>(o, iters, 1e-3f);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
       }
-      const double per_thread = op == 0 || (op >= 3 && op <= 7) ? 64.0 : 32.0;
+      const double per_thread = op == 0 || (op >= 3 && op <= 7) || op >= 9 ? 64.0 : 32.0;
       const double ops = 148.0 * th * iters * per_thread;
       printf("%-22s warps/SMSP=%d: %.3f ms  %.2f per clk per SM (at %.0f MHz)\n", names[op], th / 128, ms,
              ops / (ms * 1e-3) / (clk * 1e3) / 148, clk / 1e3);
     }
+  }
 }
