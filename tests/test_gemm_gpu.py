@@ -631,6 +631,15 @@ def test_attention_kernel_variants(variant, shape, causal, monkeypatch):
     _attn_check("f16", b, h, Q, K, V, causal)
 
 
+@pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("2", "2", "1"), ("2", "4", "1"), ("2", "1", "1")])
+def test_attention_kernel_variants_bf16_causal_ragged(variant, monkeypatch):
+    monkeypatch.setenv("CY_ATTN_KERNEL", variant[0])
+    monkeypatch.setenv("CY_ATTN_SPLIT", variant[1])
+    monkeypatch.setenv("CY_ATTN_CS", variant[2])
+    Q, K, V = _attn_inputs(1, 3, 777, 777, seed=271, dtype="bf16", qscale=4.0)
+    _attn_check("bf16", 1, 3, Q, K, V, causal=True)
+
+
 def test_attention_counts_one_launch():
     Q, K, V = _attn_inputs(1, 2, 256, 256, seed=255)
     n0 = cy.launch_count()
