@@ -174,8 +174,11 @@ __device__ __forceinline__ int blocks_for(const Params& p, int row_end) {
 // EMU of every 8 exponential pairs are evaluated with ex2_emu2.  CS = 1: warpgroup t owns query
 // tile t (one warp per row quarter); CS = 2: all 8 softmax warps work on each tile in turn, the
 // two warps of a row quarter splitting its 128 scores (two warps per SM sub-partition per tile).
+// CS = 3: like CS = 1, but the CTA has 12 warps (3 warpgroups) so that setmaxnreg can move
+// registers to the softmax warpgroups (208 each; the producer / MMA warpgroup keeps 72) and each
+// thread holds its whole 128-score row from a single TMEM pass.
 template <int DT, int EMU, int CS = 1>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const Params p) {
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int t = 0; t < NT; ++t) {
       mbar_init(bSFull + 8 * t, 1);
-      mbar_init(bPReady + 8 * t, 4 * CS);
+      mbar_init(bPReady + 8 * t, CS == 2 ? 8 : 4);
       mbar_init(bOReady + 8 * t, 1);
     }
     fence_mbar_init();
@@ -231,7 +234,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   if (threadIdx.x == 0) pdl_launch_dependents();
-
+  if (warp >= 4 * NT) {
+  // CS = 3: whole warpgroups re-balance registers at the top of each role's branch (softmax
+  // warpgroups up to 208, the producer / MMA / spare warpgroup down to 72)
+  if constexpr (CS == 3) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
   if (warp == W_PROD) {
     // ---------------------------------------------------------------- producer
     if (lane == 0 && nall > 0) {
@@ -309,6 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (next) mma_commit<1>(bKEmpty + 8 * ((j + 1) & 1), 0);  // K_{j+1} consumed
       }
     }
+  }
   } else if constexpr (CS == 2) {
     // ---------------------------------------------------------------- softmax, both tiles, split rows
     const int h = warp >> 2;        // column half: scores [64h, 64h+64), O columns [64h, 64h+64)
@@ -458,8 +465,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         p.lse[(size_t)hb * p.sq + qrow] = (lt > 0.f) ? (m[t] + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
     }
     if (lane == 0) bulk_wait_read<0>();
-  } else if (warp < 4 * NT) {
+  } else {
     // ---------------------------------------------------------------- softmax / correction / epilogue
+    if constexpr (CS == 3) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     const int t = warp >> 2;        // query tile of this warpgroup
     const int q = warp & 3;         // TMEM lane quarter
     const int r = 32 * q + lane;    // row within the tile = TMEM lane
@@ -494,9 +502,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld_wait();
       };
       // pass 1 (TMEM -> registers in 64-column groups): row max, 8 independent partial maxima
+      // (CS = 3 keeps both groups in registers for pass 2: a single TMEM pass per block)
       float mx8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+      uint32_t vrow[CS == 3 ? 2 : 1][64];
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         uint32_t v[64];
@@ -504,6 +514,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         fix(v, g);
 #pragma unroll
         for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+        if constexpr (CS == 3) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) vrow[g][e] = v[e];
+        }
       }
       float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
@@ -542,8 +556,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           uint32_t v[64];
-          load64(v, g);
-          if constexpr (E == 0) fix(v, g);
+          if constexpr (CS == 3) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) v[e] = vrow[g][e];
+          } else {
+            load64(v, g);
+            if constexpr (E == 0) fix(v, g);
+          }
           uint32_t pk[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
@@ -1144,7 +1163,7 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_attr_mu;
-bool g_attr_set[64][5][2][4] = {};
+bool g_attr_set[64][6][2][4] = {};
 
 bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r,
               bool swizzle = true) {
@@ -1238,7 +1257,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     const int v = e ? std::atoi(e) : 0;
     return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 0;
   }();
-  const void* fns[5][2][4] = {
+  const void* fns[6][2][4] = {
       {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
         (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
        {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
@@ -1258,14 +1277,21 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
       {{(const void*)&attn_fwd_kernel<0, 0, 2>, (const void*)&attn_fwd_kernel<0, 2, 2>,
         (const void*)&attn_fwd_kernel<0, 3, 2>, (const void*)&attn_fwd_kernel<0, 4, 2>},
        {(const void*)&attn_fwd_kernel<1, 0, 2>, (const void*)&attn_fwd_kernel<1, 2, 2>,
-        (const void*)&attn_fwd_kernel<1, 3, 2>, (const void*)&attn_fwd_kernel<1, 4, 2>}}};
+        (const void*)&attn_fwd_kernel<1, 3, 2>, (const void*)&attn_fwd_kernel<1, 4, 2>}},
+      {{(const void*)&attn_fwd_kernel<0, 0, 3>, (const void*)&attn_fwd_kernel<0, 2, 3>,
+        (const void*)&attn_fwd_kernel<0, 3, 3>, (const void*)&attn_fwd_kernel<0, 4, 3>},
+       {(const void*)&attn_fwd_kernel<1, 0, 3>, (const void*)&attn_fwd_kernel<1, 2, 3>,
+        (const void*)&attn_fwd_kernel<1, 3, 3>, (const void*)&attn_fwd_kernel<1, 4, 3>}}};
   const int ei = emu == 0 ? 0 : emu - 1;
-  // CY_ATTN_CS: two-tile kernel row split, 1 (one warp per row) or 2 (two warps per row, both tiles)
+  // CY_ATTN_CS: two-tile kernel softmax layout: 3 (default) one warp per row, 12 warps with
+  // setmaxnreg so each row stays in registers (one TMEM pass); 1 the same with 10 warps and two
+  // TMEM passes; 2 two warps per row, both tiles in turn
   const int cs = [] {
     const char* e = std::getenv("CY_ATTN_CS");
-    return (e && std::atoi(e) == 2) ? 2 : 1;
+    const int v = e ? std::atoi(e) : 3;
+    return (v == 1 || v == 2) ? v : 3;
   }();
-  const int ki = kern == 1 ? (cs == 2 ? 4 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
+  const int ki = kern == 1 ? (cs == 2 ? 4 : cs == 3 ? 5 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
   const void* fn = fns[ki][dt][ei];
   const int smem = kern == 2 ? pr::SMEM_BYTES : SMEM_BYTES;
   {
@@ -1293,7 +1319,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     cfg.numAttrs = 2;
   } else {
     cfg.gridDim = dim3((unsigned)((seq_q + BQ * NT - 1) / (BQ * NT)), (unsigned)bh, 1);
-    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.blockDim = dim3(cs == 3 ? 384 : THREADS, 1, 1);
     cfg.numAttrs = 1;
   }
   cfg.dynamicSmemBytes = smem;
