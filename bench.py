@@ -572,7 +572,7 @@ def main():
                                        else f"M-row shards x{world} + NCCL all-gather"),
                        "l2": "inputs rotate over 2 sets (> 126 MB L2 total)" if W["flops"] > 1e12 or args.workload == "batched" else "inputs rotate over 2 sets",
                        "kernel_config": (kinfo if args.workload != "attention" else
-                                         "attn_fwd_kernel: 2 x 128-row query tiles per CTA, 128-key blocks, TMEM S/P/O, 10 warps")},
+                                         "attn_fwd_kernel: 2 x 128-row query tiles per CTA, 128-key blocks, TMEM S/P/O, 12 warps (setmaxnreg 208/72)")},
             "pct_of_dense_peak": round(100.0 * value / world / peak, 2),
             "pct_of_nominal_2250": round(100.0 * value / world / 2250.0, 2),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
