@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -647,6 +648,340 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
 }
 
 
+
+// ============================================================================ persistent two-tile kernel
+// The default layout (two 128-row query tiles per CTA, softmax warpgroup per tile, setmaxnreg)
+// made persistent: one CTA per SM walks the work items (query-tile pair, batch*head) -- the
+// "persistent kernel" optimisation the paper names as Cypress's missing piece for attention
+// (P:1657-1664).  Across items the K/V rings and every barrier phase simply continue; the O_t
+// accumulator is handed back by the epilogue (bOFree_t) before the next item's first PV_t, and the
+// next item's Q tiles load as soon as the last S MMAs of the previous item have read Q (bQEmpty),
+// so one item's epilogue overlaps the next item's loads, first S MMAs and first softmax.
+// Shared: Q 2 x 32 KB, K/V 2 x 64 KB, O staging 8 x 4 KB (no longer aliased with Q).
+constexpr int PS_STAGE_OFF = (NT + 4) * TILE;                 // 8 warps x 4 KB epilogue staging
+constexpr int PS_BAR_OFF = PS_STAGE_OFF + 8 * 4096;
+constexpr int PS_SMEM_BYTES = 1024 + PS_BAR_OFF + 256;
+
+__device__ __forceinline__ void item_coords(const Params& p, int item, int nq, int& qt, int& hb) {
+  // query tiles fastest, as in the one-CTA-per-item grid: the items in flight share a few heads'
+  // K/V, which stay in L2 and whose TMA requests merge
+  hb = item / nq;
+  const int qi = item - hb * nq;
+  qt = p.causal ? (nq - 1 - qi) : qi;  // causal: heaviest query tile of each head first
+}
+
+template <int DT>
+__global__ void __launch_bounds__(384, 1)
+    attn_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                        const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sQ = base + SQ_OFF, sK = base + SK_OFF, sV = base + SV_OFF, sStage = base + PS_STAGE_OFF;
+  const uint32_t bar = base + PS_BAR_OFF;
+  const uint32_t bQFull = bar, bQEmpty = bar + 8, bKFull = bar + 16, bKEmpty = bar + 32, bVFull = bar + 48,
+                 bVEmpty = bar + 64, bSFull = bar + 80, bPReady = bar + 96, bOReady = bar + 112, bOFree = bar + 128,
+                 sTmemSlot = bar + 144;
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nq = (p.sq + BQ * NT - 1) / (BQ * NT);
+  const int items = nq * p.bh;
+  auto blocks_of = [&](int qt, int t) { return blocks_for(p, qt * BQ * NT + BQ * (t + 1)); };
+
+  if (warp == W_PROD && lane == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    prefetch_tmap(&tmO);
+    mbar_init(bQFull, 1);
+    mbar_init(bQEmpty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bKFull + 8 * s, 1);
+      mbar_init(bKEmpty + 8 * s, 1);
+      mbar_init(bVFull + 8 * s, 1);
+      mbar_init(bVEmpty + 8 * s, 1);
+    }
+    for (int t = 0; t < NT; ++t) {
+      mbar_init(bSFull + 8 * t, 1);
+      mbar_init(bPReady + 8 * t, 4);
+      mbar_init(bOReady + 8 * t, 1);
+      mbar_init(bOFree + 8 * t, 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == W_MMA) {
+    tmem_alloc<1>(sTmemSlot, 512);
+    tmem_relinquish<1>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  if (threadIdx.x == 0) pdl_launch_dependents();
+
+  if (warp >= 4 * NT) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+    if (warp == W_PROD && lane == 0) {
+      // ---------------------------------------------------------------- producer
+      const uint64_t pol = policy_evict_last();
+      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t b, int c0, int c1, int hb) {
+        if (p.l2hint) tma_load_3d(dst, tm, b, c0, c1, hb, pol);
+        else tma_load_3d_nohint(dst, tm, b, c0, c1, hb);
+      };
+      int g = 0;  // K/V blocks loaded so far (ring position across items)
+      int it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        int qt, hb;
+        item_coords(p, item, nq, qt, hb);
+        const int nall = blocks_of(qt, NT - 1);
+        if (nall == 0) continue;
+        if (it > 0) mbar_wait(bQEmpty, (it - 1) & 1);  // the previous item's S MMAs have read Q
+        mbar_arrive_expect_tx(bQFull, NT * TILE);
+        for (int t = 0; t < NT; ++t) {
+          ld(sQ + t * TILE, &tmQ, bQFull, 0, qt * BQ * NT + BQ * t, hb);
+          ld(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, qt * BQ * NT + BQ * t, hb);
+        }
+        for (int j = 0; j < nall; ++j, ++g) {
+          const int s = g & 1;
+          const int k0 = j * BKV;
+          mbar_wait(bKEmpty + 8 * s, ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(bKFull + 8 * s, TILE);
+          ld(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0, hb);
+          ld(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0, hb);
+          mbar_wait(bVEmpty + 8 * s, ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(bVFull + 8 * s, TILE);
+          ld(sV + s * TILE, &tmV, bVFull + 8 * s, 0, k0, hb);
+          ld(sV + s * TILE + ATOM, &tmV, bVFull + 8 * s, 64, k0, hb);
+        }
+      }
+    } else if (warp == W_MMA && lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      constexpr uint32_t ID_S = idesc<DT, false>(), ID_PV = idesc<DT, true>();
+      int g = 0;            // K/V ring position
+      int gt[NT] = {0, 0};  // blocks issued per tile so far (S / P / O barrier phases)
+      int it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        int qt, hb;
+        item_coords(p, item, nq, qt, hb);
+        int nkv[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) nkv[t] = blocks_of(qt, t);
+        const int nall = nkv[NT - 1];
+        if (nall == 0) continue;
+        auto issue_s = [&](int t, int j) {
+          const uint32_t k = sK + ((g + j) & 1) * TILE, q = sQ + t * TILE;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+            mma_f16<1>(tmem + TM_S + t * 128, sdesc_sw128(q + off, 16, 1024), sdesc_sw128(k + off, 16, 1024), ID_S,
+                       kk > 0);
+          }
+          mma_commit<1>(bSFull + 8 * t, 0);
+        };
+        auto issue_pv = [&](int t, int j) {
+          mbar_wait(bPReady + 8 * t, (gt[t] + j) & 1);
+          tc_fence_after();
+          const uint32_t v = sV + ((g + j) & 1) * TILE;
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + kk * 8, sdesc_sw128(v + kk * 2048, ATOM, 1024),
+                       ID_PV, (j | kk) != 0);
+          mma_commit<1>(bOReady + 8 * t, 0);
+        };
+        mbar_wait(bQFull, it & 1);
+        mbar_wait(bKFull + 8 * (g & 1), (g >> 1) & 1);
+        tc_fence_after();
+        for (int t = 0; t < NT; ++t)
+          if (nkv[t] > 0) issue_s(t, 0);
+        mma_commit<1>(bKEmpty + 8 * (g & 1), 0);
+        if (nall == 1) mma_commit<1>(bQEmpty, 0);  // Q read for the last time
+        for (int j = 0; j < nall; ++j) {
+          const bool next = j + 1 < nall;
+          if (next) {
+            mbar_wait(bKFull + 8 * ((g + j + 1) & 1), ((g + j + 1) >> 1) & 1);
+            tc_fence_after();
+          }
+          mbar_wait(bVFull + 8 * ((g + j) & 1), ((g + j) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (j < nkv[t]) {
+              if (j == 0 && it > 0) {  // O_t of the previous item has been read by its epilogue
+                mbar_wait(bOFree + 8 * t, (it - 1) & 1);
+                tc_fence_after();
+              }
+              issue_pv(t, j);
+            }
+            if (t == NT - 1) mma_commit<1>(bVEmpty + 8 * ((g + j) & 1), 0);
+            if (next && j + 1 < nkv[t]) issue_s(t, j + 1);
+          }
+          if (next) {
+            mma_commit<1>(bKEmpty + 8 * ((g + j + 1) & 1), 0);
+            if (j + 2 == nall) mma_commit<1>(bQEmpty, 0);  // the last S MMAs of this item are issued
+          }
+        }
+        g += nall;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) gt[t] += nkv[t];
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax / epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    const int t = warp >> 2;
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const uint32_t tS = tmem + lane_base + TM_S + t * 128;
+    const uint32_t tO = tmem + lane_base + TM_O + t * 128;
+    const uint32_t sE = sStage + warp * 4096;
+    int gt = 0;  // this tile's blocks so far (barrier phases)
+    int it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      int qt, hb;
+      item_coords(p, item, nq, qt, hb);
+      if (blocks_of(qt, NT - 1) == 0) continue;  // (sk == 0 is handled on the host)
+      const int nk = blocks_of(qt, t);
+      const int trow0 = qt * BQ * NT + BQ * t;
+      const int qrow = trow0 + r;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nk; ++j) {
+        mbar_wait(bSFull + 8 * t, (gt + j) & 1);
+        if (j > 0) mbar_wait(bOReady + 8 * t, (gt + j - 1) & 1);  // never blocks (in-order tcgen05)
+        tc_fence_after();
+        const int key0 = j * BKV;
+        const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= trow0);
+        uint32_t vrow[2][64];
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          tmem_ld_32x32b_x32(tS + 64 * gg, *reinterpret_cast<uint32_t(*)[32]>(&vrow[gg][0]));
+          tmem_ld_32x32b_x32(tS + 64 * gg + 32, *reinterpret_cast<uint32_t(*)[32]>(&vrow[gg][32]));
+        }
+        tmem_ld_wait();
+        if (!full_block) {
+#pragma unroll
+          for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+            for (int e = 0; e < 64; ++e) {
+              const int key = key0 + 64 * gg + e;
+              if (key >= p.sk || (p.causal && key > qrow)) vrow[gg][e] = __float_as_uint(-INFINITY);
+            }
+        }
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(vrow[gg][e]));
+        float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;
+        float m_new = m, corr = 1.f;
+        if (mb > m + 8.f) {
+          m_new = mb;
+          corr = ex2(m - m_new);
+        }
+        const float msub = (m_new == -INFINITY) ? 0.f : m_new;
+        if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x32(tO + 32 * c, o);
+          }
+        }
+        float2 sm4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 ms2 = make_float2(-msub, -msub);
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float2 x =
+                ffma2(make_float2(__uint_as_float(vrow[gg][2 * e]), __uint_as_float(vrow[gg][2 * e + 1])), sc2, ms2);
+            float2 pe;
+            pe.x = ex2(x.x);
+            pe.y = ex2(x.y);
+            sm4[e & 3] = fadd2(sm4[e & 3], pe);
+            pk[e] = pack2<DT>(pe.x, pe.y);
+          }
+          tmem_st_32x32b_x32(tS + 32 * gg, pk);  // P over columns [0, 64) (scores already in registers)
+        }
+        tmem_st_wait();
+        l = l * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
+                        ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
+        m = m_new;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bPReady + 8 * t);
+      }
+      // ---------------------------------------------------------------- epilogue of this item
+      const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+      if (nk > 0) {
+        mbar_wait(bOReady + 8 * t, (gt + nk - 1) & 1);
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t a0[32], a1[32];
+        if (nk > 0) {
+          tmem_ld_32x32b_x32(tO + 64 * c, a0);
+          tmem_ld_32x32b_x32(tO + 64 * c + 32, a1);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) a0[e] = a1[e] = 0u;
+        }
+        if (c == 1) {  // O_t is in registers: the next item's first PV_t may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bOFree + 8 * t);
+        }
+        if (lane == 0) bulk_wait_read<0>();  // the staging buffer's previous store has read it
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int col = 8 * v + 2 * u;
+            const float x0 = __uint_as_float(col < 32 ? a0[col] : a1[col - 32]) * inv_l;
+            const float x1 = __uint_as_float(col + 1 < 32 ? a0[col + 1] : a1[col + 1 - 32]) * inv_l;
+            w[u] = pack2<DT>(x0, x1);
+          }
+          st_shared_v4(sE + lane * 128 + ((v ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmO, sE, 64 * c, trow0 + 32 * q, hb);
+          bulk_commit();
+        }
+      }
+      if (p.lse && qrow < p.sq)
+        p.lse[(size_t)hb * p.sq + qrow] = (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      gt += nk;
+    }
+    if (lane == 0) bulk_wait_read<0>();
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, 512);
+  }
+}
+
 // ============================================================================ CTA-pair kernel
 // Two CTAs of a cluster own 256 consecutive query rows of one (batch, head), 128 rows each, and
 // issue every MMA as one cta_group::2 instruction (M = 256): the leader's MMA thread computes
@@ -1163,7 +1498,8 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_attr_mu;
-bool g_attr_set[64][6][2][4] = {};
+bool g_attr_set[64][7][2][4] = {};
+int g_sms[64] = {};
 
 bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r,
               bool swizzle = true) {
@@ -1257,7 +1593,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     const int v = e ? std::atoi(e) : 0;
     return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 0;
   }();
-  const void* fns[6][2][4] = {
+  const void* fns[7][2][4] = {
       {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
         (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
        {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
@@ -1281,7 +1617,9 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
       {{(const void*)&attn_fwd_kernel<0, 0, 3>, (const void*)&attn_fwd_kernel<0, 2, 3>,
         (const void*)&attn_fwd_kernel<0, 3, 3>, (const void*)&attn_fwd_kernel<0, 4, 3>},
        {(const void*)&attn_fwd_kernel<1, 0, 3>, (const void*)&attn_fwd_kernel<1, 2, 3>,
-        (const void*)&attn_fwd_kernel<1, 3, 3>, (const void*)&attn_fwd_kernel<1, 4, 3>}}};
+        (const void*)&attn_fwd_kernel<1, 3, 3>, (const void*)&attn_fwd_kernel<1, 4, 3>}},
+      {{(const void*)&attn_persist_kernel<0>, nullptr, nullptr, nullptr},
+       {(const void*)&attn_persist_kernel<1>, nullptr, nullptr, nullptr}}};
   const int ei = emu == 0 ? 0 : emu - 1;
   // CY_ATTN_CS: two-tile kernel softmax layout: 3 (default) one warp per row, 12 warps with
   // setmaxnreg so each row stays in registers (one TMEM pass); 1 the same with 10 warps and two
@@ -1291,9 +1629,17 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     const int v = e ? std::atoi(e) : 3;
     return (v == 1 || v == 2) ? v : 3;
   }();
-  const int ki = kern == 1 ? (cs == 2 ? 4 : cs == 3 ? 5 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
-  const void* fn = fns[ki][dt][ei];
-  const int smem = kern == 2 ? pr::SMEM_BYTES : SMEM_BYTES;
+  // CY_ATTN_PERSIST=1: the default layout as a persistent kernel (one CTA per SM walking the work
+  // items, static round-robin).  Measured -2 % non-causal at 8192, +2 % at 2048, -8..12 % causal
+  // (static schedule, uneven items), so off by default.  Not used with EMU or seq_k == 0.
+  const int persist = [] {
+    const char* e = std::getenv("CY_ATTN_PERSIST");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool ps = kern == 1 && cs == 3 && emu == 0 && persist && seq_k > 0;
+  const int ki = ps ? 6 : kern == 1 ? (cs == 2 ? 4 : cs == 3 ? 5 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
+  const void* fn = fns[ki][dt][ps ? 0 : ei];
+  const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : SMEM_BYTES;
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     if (!g_attr_set[dev][ki][dt][ei]) {
@@ -1303,6 +1649,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
       }
       g_attr_set[dev][ki][dt][ei] = true;
     }
+    if (g_sms[dev] == 0) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
   }
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
@@ -1317,6 +1664,11 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     attrs[1].val.clusterDim.y = 1;
     attrs[1].val.clusterDim.z = 1;
     cfg.numAttrs = 2;
+  } else if (ps) {
+    const int64_t items = ((seq_q + BQ * NT - 1) / (BQ * NT)) * bh;
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(items, std::max(1, g_sms[dev])), 1, 1);
+    cfg.blockDim = dim3(384, 1, 1);
+    cfg.numAttrs = 1;
   } else {
     cfg.gridDim = dim3((unsigned)((seq_q + BQ * NT - 1) / (BQ * NT)), (unsigned)bh, 1);
     cfg.blockDim = dim3(cs == 3 ? 384 : THREADS, 1, 1);

@@ -618,7 +618,8 @@ def test_attention_closed_forms():
     assert_bits_equal(to_bits(O1).reshape(2, 7, d), np.repeat(V[:, :1], 7, axis=1), "one key")
 
 
-@pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("1", "2", "3"), ("2", "2", "1"), ("2", "4", "1"), ("2", "1", "1")])
+@pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("1", "2", "3"), ("1", "2", "3", "1"), ("2", "2", "1"),
+                                     ("2", "4", "1"), ("2", "1", "1")])
 @pytest.mark.parametrize("shape,causal", [((1, 2, 300, 500), False), ((2, 1, 640, 640), True), ((1, 3, 129, 257), False),
                                           ((1, 1, 1, 1), False), ((1, 2, 1024, 1024), True)])
 def test_attention_kernel_variants(variant, shape, causal, monkeypatch):
@@ -626,16 +627,19 @@ def test_attention_kernel_variants(variant, shape, causal, monkeypatch):
     monkeypatch.setenv("CY_ATTN_KERNEL", variant[0])
     monkeypatch.setenv("CY_ATTN_SPLIT", variant[1])
     monkeypatch.setenv("CY_ATTN_CS", variant[2])
+    monkeypatch.setenv("CY_ATTN_PERSIST", variant[3] if len(variant) > 3 else "0")
     b, h, sq, sk = shape
     Q, K, V = _attn_inputs(b, h, sq, sk, seed=261 + sq + sk, qscale=4.0)
     _attn_check("f16", b, h, Q, K, V, causal)
 
 
-@pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("1", "2", "3"), ("2", "2", "1"), ("2", "4", "1"), ("2", "1", "1")])
+@pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("1", "2", "3"), ("1", "2", "3", "1"), ("2", "2", "1"),
+                                     ("2", "4", "1"), ("2", "1", "1")])
 def test_attention_kernel_variants_bf16_causal_ragged(variant, monkeypatch):
     monkeypatch.setenv("CY_ATTN_KERNEL", variant[0])
     monkeypatch.setenv("CY_ATTN_SPLIT", variant[1])
     monkeypatch.setenv("CY_ATTN_CS", variant[2])
+    monkeypatch.setenv("CY_ATTN_PERSIST", variant[3] if len(variant) > 3 else "0")
     Q, K, V = _attn_inputs(1, 3, 777, 777, seed=271, dtype="bf16", qscale=4.0)
     _attn_check("bf16", 1, 3, Q, K, V, causal=True)
 
