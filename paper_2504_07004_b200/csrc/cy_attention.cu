@@ -42,6 +42,9 @@ void note_launch();  // cy_gemm.cu: the library-wide launch counter behind cy_la
 namespace cy_attn {
 using namespace cy;
 
+#ifndef CY_ATTN_PH_E
+#define CY_ATTN_PH_E 7
+#endif
 constexpr int D = 128;        // head dim (the paper's configuration)
 constexpr int BQ = 128;       // query rows per tile (TMEM lanes)
 constexpr int NT = 2;         // query tiles per CTA (two softmax warpgroups ping-pong on the tensor core)
@@ -192,6 +195,9 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
   // PV(j), so each refill starts as soon as its own readers are done
   const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bar + 24, bVFull = bar + 40, bVEmpty = bar + 56,
                  bSFull = bar + 72, bPReady = bar + 88, bOReady = bar + 104, sTmemSlot = bar + 120;
+  // CS = 3: P_t for keys [0, 64) of the block is published first (bPHalf), so the tensor core starts
+  // the first half of PV_t(j) while the softmax warps still compute the second half of P_t
+  const uint32_t bPHalf = bar + 128;
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,6 +228,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
       mbar_init(bSFull + 8 * t, 1);
       mbar_init(bPReady + 8 * t, CS == 2 ? 8 : 4);
       mbar_init(bOReady + 8 * t, 1);
+      mbar_init(bPHalf + 8 * t, 4);
     }
     fence_mbar_init();
   }
@@ -282,13 +289,24 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         mma_commit<1>(bSFull + 8 * t, 0);
       };
       auto issue_pv = [&](int t, int j) {
-        mbar_wait(bPReady + 8 * t, j & 1);
-        tc_fence_after();
         const uint32_t v = sV + (j & 1) * TILE;
         // O_t += P_t V_j: P_t read from TMEM (packed 16-bit pairs over S_t, 8 columns per k16 step);
         // S_t(j+1) is issued after this and tcgen05 ops execute in order, so it cannot clobber P_t.
+        // CS = 3: the first four k16 steps (keys [0, 64), P columns [0, 32)) go as soon as that half
+        // of P_t is in TMEM.
+        constexpr int KK0 = (CS == 3) ? BKV / 32 : 0;
+        if constexpr (CS == 3) {
+          mbar_wait(bPHalf + 8 * t, j & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
+          for (int kk = 0; kk < KK0; ++kk)
+            mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8,
+                       sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV, (j | kk) != 0);
+        }
+        mbar_wait(bPReady + 8 * t, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = KK0; kk < BKV / 16; ++kk)
           mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8,
                      sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV, (j | kk) != 0);
         mma_commit<1>(bOReady + 8 * t, 0);
@@ -508,16 +526,28 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
       uint32_t vrow[CS == 3 ? 2 : 1][64];
+      if constexpr (CS == 3) {
+        // the whole row in flight at once: four loads behind a single wait
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        uint32_t v[64];
-        load64(v, g);
-        fix(v, g);
+        for (int g = 0; g < 2; ++g) {
+          tmem_ld_32x32b_x32(tS + 64 * g, *reinterpret_cast<uint32_t(*)[32]>(&vrow[g][0]));
+          tmem_ld_32x32b_x32(tS + 64 * g + 32, *reinterpret_cast<uint32_t(*)[32]>(&vrow[g][32]));
+        }
+        tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
-        if constexpr (CS == 3) {
+        for (int g = 0; g < 2; ++g) {
+          fix(vrow[g], g);
 #pragma unroll
-          for (int e = 0; e < 64; ++e) vrow[g][e] = v[e];
+          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(vrow[g][e]));
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          uint32_t v[64];
+          load64(v, g);
+          fix(v, g);
+#pragma unroll
+          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
         }
       }
       float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
@@ -577,6 +607,15 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
             }
             sm4[e & 3] = fadd2(sm4[e & 3], pe);
             pk[e] = pack2<DT>(pe.x, pe.y);
+            if constexpr (CS == 3) {
+              if (g == 1 && e == CY_ATTN_PH_E) {
+                // group 0's P (and any O rescale) has long been stored: publish the first half
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bPHalf + 8 * t);
+              }
+            }
           }
           // group 1's P lands in columns 32..63, which group 1's scores (columns 64..127) do not
           // overlap; group 0's P (columns 0..31) overwrites scores already consumed
