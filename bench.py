@@ -34,6 +34,13 @@ METRIC = "fp16 GEMM TFLOP/s per B200 and % of dense tensor peak; 8-GPU aggregate
 ATTN_METRIC = "fp16 flash-attention forward TFLOP/s (HeadDim 128, 4*b*h*s^2*d FLOP)"
 
 
+def scaling_of(workload):
+    """'weak' when every rank's work is fixed as N grows (gemm: 8192 rows per GPU; sweep-n: n rows per
+    GPU; attention: batch 2 per GPU), 'strong' when the total problem is fixed and split over the
+    ranks (batched 64 x 1024^3, rowreduce/allgather 65536 rows, dual/glu 8192^3)."""
+    return "strong" if workload in ("batched", "rowreduce", "allgather", "dual", "glu") else "weak"
+
+
 def metric_for(workload):
     return ATTN_METRIC if workload == "attention" else METRIC
 
@@ -564,7 +571,7 @@ def main():
         out = {
             "metric": metric_for(args.workload), "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "scaling": scaling_of(args.workload), "vs_baseline": None, "dtype": "f16",
             "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
             "config": {"workload": W["desc"], **W["shape"],
                        "parallelism": (f"batch shards x{world}, no collective" if args.workload in ("batched", "attention")
@@ -630,12 +637,13 @@ def reference_arm(args, rank, world):
     elif name == "batched":
         A = synth.uniform((64, 1024, 1024), synth.seed_for(2, 0))
         B = synth.uniform((64, 1024, 1024), synth.seed_for(2, 1))
-        per_row = 2.0 * 1024 * 1024
-        m = 64 * 1024
+        # sample unit = one whole 1024^3 GEMM of the batch (as the bench's cpu_baseline does)
+        per_row = 2.0 * 1024 ** 3
+        m = 64
 
         def fn(rows):
-            for r in np.unique(rows // 1024):
-                oracle.gemm("f16", A[r], B[r], rows=rows[rows // 1024 == r] % 1024)
+            for r in rows:
+                oracle.gemm("f16", A[r], B[r])
         desc = "batched fp16 GEMM 64 x 1024^3"
     elif name == "glu":
         n = 8192
@@ -661,7 +669,7 @@ def reference_arm(args, rank, world):
         value = statistics.mean(v["value"] for v in vals)
         out = {"impl": "reference", "metric": ATTN_METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
                "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "scaling": scaling_of(name), "vs_baseline": None, "dtype": "f64",
                "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
                "config": {"workload": desc, "parallelism": "CPU oracle, rank 0 only"},
                "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": vals[0]["cores"], "kind": "oracle",
@@ -697,10 +705,11 @@ def reference_arm(args, rank, world):
         fn(np.sort(rng.choice(m, rows_per_step, replace=False)))
     dt = time.perf_counter() - t0
     value = per_row * rows_per_step * steps / dt / 1e12
-    sample = f"{rows_per_step} random rows (all columns, full K) per step of {desc}; {steps} steps in {dt:.1f} s"
+    unit = "random batch GEMMs (1024^3 each)" if name == "batched" else "random rows (all columns, full K)"
+    sample = f"{rows_per_step} {unit} per step of {desc}; {steps} steps in {dt:.1f} s"
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "scaling": scaling_of(name), "vs_baseline": None, "dtype": "f64",
            "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
            "config": {"workload": desc, "parallelism": "CPU oracle, rank 0 only"},
            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": nth, "kind": "oracle", "sample": sample},
