@@ -45,6 +45,33 @@ using namespace cy;
 #ifndef CY_ATTN_PH_E
 #define CY_ATTN_PH_E 7
 #endif
+// Build knobs of the CS = 3 kernel (experiments; the defaults are the measured best):
+// CY_ATTN_PH_E: pair index of the second P group after which the first half of P_t is published.
+// CY_ATTN_PP: softmax ping-pong: 0 off; 1 the two tiles' exponential passes strictly alternate (named
+// barriers 8 / 9); 2 the whole per-block softmax alternates.  Measured: 1 on par, 2 -5 %.
+#ifndef CY_ATTN_PP
+#define CY_ATTN_PP 0
+#endif
+// CY_ATTN_PF: K/V L2 prefetch distance in blocks (0 = off).  A K/V tile takes ~4-5 K cycles from
+// TMA issue to full barrier inside the kernel (CY_ATTN_TRACE), but that is the closed loop of the
+// rings, not L2 latency: prefetching 2-6 blocks ahead measured -1..-2 %, and skipping the K/V
+// reloads altogether (CY_ATTN_DBG_NOLOAD, invalid results) only +5 %.
+#ifndef CY_ATTN_PF
+#define CY_ATTN_PF 0
+#endif
+// CY_ATTN_TRACE (timing experiments only, never in the product build): clock64() stamps of one
+// CTA's per-block events, read back with cy_attn_trace()
+#ifdef CY_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[16 * 2 * 64];
+#define ATRACE(cond, ev, t, j)                                                                       \
+  do {                                                                                              \
+    if ((cond) && blockIdx.x == 3 && blockIdx.y == 5 && (j) < 64) g_attn_trace[((ev) * 2 + (t)) * 64 + (j)] = clock64(); \
+  } while (0)
+#else
+#define ATRACE(cond, ev, t, j) \
+  do {                         \
+  } while (0)
+#endif
 constexpr int D = 128;        // head dim (the paper's configuration)
 constexpr int BQ = 128;       // query rows per tile (TMEM lanes)
 constexpr int NT = 2;         // query tiles per CTA (two softmax warpgroups ping-pong on the tensor core)
@@ -57,6 +84,15 @@ constexpr int SV_OFF = (NT + 2) * TILE;    // [2]
 constexpr int BAR_OFF = (NT + 4) * TILE;
 constexpr int XCH_OFF = BAR_OFF + 256;       // CS = 2: row-max exchange [NT][2][2][BQ], sums [NT][2][BQ]
 constexpr int SMEM_BYTES = 1024 + (NT + 4) * TILE + 256 + (NT * 2 * 2 * BQ + NT * 2 * BQ) * 4;
+// CS = 3 layout: V gets a third ring slot (a K/V tile load takes ~4-5 K cycles under load, longer than
+// the lead two slots give); barriers after the last V slot, no exchange area
+#ifndef CY_ATTN_VS3
+#define CY_ATTN_VS3 3
+#endif
+constexpr int VS3 = CY_ATTN_VS3;
+constexpr int BAR_OFF3 = (NT + 2 + VS3) * TILE;
+constexpr int SMEM_BYTES3 = 1024 + BAR_OFF3 + 256;
+static_assert(SMEM_BYTES3 <= 232448, "CS = 3 layout exceeds 227 KB");
 constexpr int THREADS = (4 * NT + 2) * 32;  // softmax warpgroups 0..NT-1, then producer, MMA issuer
 constexpr int W_PROD = 4 * NT, W_MMA = 4 * NT + 1;
 constexpr uint32_t TM_S = 0, TM_O = 256;   // S_t at 128 t, O_t at 256 + 128 t
@@ -190,11 +226,13 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   const uint32_t sQ = base + SQ_OFF, sK = base + SK_OFF, sV = base + SV_OFF;
-  const uint32_t bar = base + BAR_OFF;
+  constexpr int VS = (CS == 3) ? VS3 : 2;  // V ring slots
+  const uint32_t bar = base + (CS == 3 ? BAR_OFF3 : BAR_OFF);
   // K and V have separate 2-slot rings: K_j is released after the last S(j), V_j after the last
   // PV(j), so each refill starts as soon as its own readers are done
-  const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bar + 24, bVFull = bar + 40, bVEmpty = bar + 56,
-                 bSFull = bar + 72, bPReady = bar + 88, bOReady = bar + 104, sTmemSlot = bar + 120;
+  const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bar + 24, bSFull = bar + 72, bPReady = bar + 88,
+                 bOReady = bar + 104, sTmemSlot = bar + 120;
+  const uint32_t bVFull = (VS == 2) ? bar + 40 : bar + 144, bVEmpty = (VS == 2) ? bar + 56 : bar + 144 + 8 * VS;
   // CS = 3: P_t for keys [0, 64) of the block is published first (bPHalf), so the tensor core starts
   // the first half of PV_t(j) while the softmax warps still compute the second half of P_t
   const uint32_t bPHalf = bar + 128;
@@ -221,6 +259,8 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(bKFull + 8 * s, 1);
       mbar_init(bKEmpty + 8 * s, 1);
+    }
+    for (int s = 0; s < VS; ++s) {
       mbar_init(bVFull + 8 * s, 1);
       mbar_init(bVEmpty + 8 * s, 1);
     }
@@ -259,17 +299,42 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         ld(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t);
         ld(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, q0 + BQ * t);
       }
+      auto prefetch_kv = [&](int jb) {
+        if (jb < nall) {
+          tma_prefetch_3d(&tmK, 0, jb * BKV, hb);
+          tma_prefetch_3d(&tmK, 64, jb * BKV, hb);
+          tma_prefetch_3d(&tmV, 0, jb * BKV, hb);
+          tma_prefetch_3d(&tmV, 64, jb * BKV, hb);
+        }
+      };
+      if constexpr (CY_ATTN_PF > 0)
+        for (int jb = 2; jb < CY_ATTN_PF; ++jb) prefetch_kv(jb);
       for (int j = 0; j < nall; ++j) {
         const int s = j & 1;
         const int k0 = j * BKV;
+        if constexpr (CY_ATTN_PF > 0)
+          if (j + CY_ATTN_PF >= 2) prefetch_kv(j + CY_ATTN_PF);
         mbar_wait(bKEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
+        ATRACE(true, 8, 0, j);
+#ifdef CY_ATTN_DBG_NOLOAD
+        // timing experiment only (invalid results): K/V tiles after the first ring fill are not reloaded
+        if (j >= 4) {
+          mbar_arrive(bKFull + 8 * s);
+          const int vs = j % VS;
+          mbar_wait(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
+          mbar_arrive(bVFull + 8 * vs);
+          continue;
+        }
+#endif
         mbar_arrive_expect_tx(bKFull + 8 * s, TILE);
         ld(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0);
         ld(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0);
-        mbar_wait(bVEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(bVFull + 8 * s, TILE);
-        ld(sV + s * TILE, &tmV, bVFull + 8 * s, 0, k0);
-        ld(sV + s * TILE + ATOM, &tmV, bVFull + 8 * s, 64, k0);
+        const int vs = j % VS;
+        mbar_wait(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
+        ATRACE(true, 9, 0, j);
+        mbar_arrive_expect_tx(bVFull + 8 * vs, TILE);
+        ld(sV + vs * TILE, &tmV, bVFull + 8 * vs, 0, k0);
+        ld(sV + vs * TILE + ATOM, &tmV, bVFull + 8 * vs, 64, k0);
       }
     }
   } else if (warp == W_MMA) {
@@ -289,7 +354,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         mma_commit<1>(bSFull + 8 * t, 0);
       };
       auto issue_pv = [&](int t, int j) {
-        const uint32_t v = sV + (j & 1) * TILE;
+        const uint32_t v = sV + (j % VS) * TILE;
         // O_t += P_t V_j: P_t read from TMEM (packed 16-bit pairs over S_t, 8 columns per k16 step);
         // S_t(j+1) is issued after this and tcgen05 ops execute in order, so it cannot clobber P_t.
         // CS = 3: the first four k16 steps (keys [0, 64), P columns [0, 32)) go as soon as that half
@@ -297,6 +362,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         constexpr int KK0 = (CS == 3) ? BKV / 32 : 0;
         if constexpr (CS == 3) {
           mbar_wait(bPHalf + 8 * t, j & 1);
+          ATRACE(true, 4, t, j);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < KK0; ++kk)
@@ -304,6 +370,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
                        sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV, (j | kk) != 0);
         }
         mbar_wait(bPReady + 8 * t, j & 1);
+        ATRACE(true, 5, t, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = KK0; kk < BKV / 16; ++kk)
@@ -319,17 +386,30 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
       mma_commit<1>(bKEmpty, 0);  // K_0 consumed
       for (int j = 0; j < nall; ++j) {
         const bool next = j + 1 < nall;
-        if (next) {
-          mbar_wait(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
-          tc_fence_after();
-        }
-        mbar_wait(bVFull + 8 * (j & 1), (j >> 1) & 1);
+        // operands are awaited where they are first read: V_j before PV_0(j), K_{j+1} only before
+        // S_0(j+1), so PV_0(j) runs while K_{j+1} is still landing
+        bool k_ready = !next;
+        mbar_wait(bVFull + 8 * (j % VS), (j / VS) & 1);
+        ATRACE(true, 7, 0, j);
         tc_fence_after();
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           if (j < nkv[t]) issue_pv(t, j);
-          if (t == NT - 1) mma_commit<1>(bVEmpty + 8 * (j & 1), 0);  // V_j fully consumed
-          if (next && j + 1 < nkv[t]) issue_s(t, j + 1);
+          if (t == NT - 1) mma_commit<1>(bVEmpty + 8 * (j % VS), 0);  // V_j fully consumed
+          if (next && j + 1 < nkv[t]) {
+            if (!k_ready) {
+              mbar_wait(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
+              ATRACE(true, 10, 0, j + 1);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_s(t, j + 1);
+            ATRACE(true, 6, t, j + 1);
+          }
+        }
+        if (!k_ready) {  // no S this iteration (causal tail): still consume the phase
+          mbar_wait(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
+          tc_fence_after();
         }
         if (next) mma_commit<1>(bKEmpty + 8 * ((j + 1) & 1), 0);  // K_{j+1} consumed
       }
@@ -497,8 +577,25 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
     const uint32_t tS = tmem + lane_base + TM_S + t * 128;
     const uint32_t tO = tmem + lane_base + TM_O + t * 128;
     float m = -INFINITY, l = 0.f;
+    // Ping-pong of the two softmax warpgroups (CS = 3): both tiles need the SFU at the same rate as
+    // the tensor core, so their exponential passes take turns -- tile 0 block j, tile 1 block j,
+    // tile 0 block j+1, ... -- and each runs at the full SFU rate while the tensor core computes
+    // the other tile's PV and S.  Named barrier 8 + t = "tile t may start"; tile 1 only waits while
+    // tile 0 still has blocks (causal tiles: nkv[0] <= nkv[1]).
+    auto pp_wait = [&](int j) {
+      if constexpr (CS == 3 && CY_ATTN_PP > 0)
+        if (t == 0 ? j > 0 : j < nkv[0]) asm volatile("bar.sync %0, 256;" ::"r"(8 + t) : "memory");
+    };
+    auto pp_pass = [&](int j) {
+      if constexpr (CS == 3 && CY_ATTN_PP > 0)
+        if (t == 0 || j + 1 < nkv[0]) asm volatile("bar.arrive %0, 256;" ::"r"(9 - t) : "memory");
+    };
+    const bool tr = (threadIdx.x & 127) == 0;
+    (void)tr;
     for (int j = 0; j < nk; ++j) {
       mbar_wait(bSFull + 8 * t, j & 1);
+      ATRACE(tr, 0, t, j);
+      if constexpr (CY_ATTN_PP == 2) pp_wait(j);
       // PV_t(j-1) was issued before S_t(j) and tcgen05 ops complete in order, so this never blocks;
       // consuming every phase keeps the barrier protocol explicit (and compute-sanitizer clean)
       if (j > 0) mbar_wait(bOReady + 8 * t, (j - 1) & 1);
@@ -622,10 +719,14 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
           tmem_st_32x32b_x32(tS + 32 * g, pk);
         }
       };
+      ATRACE(tr, 1, t, j);
+      if constexpr (CY_ATTN_PP == 1) pp_wait(j);
       if (EMU > 0 && full_block)
         pass2(std::integral_constant<int, EMU>{});
       else
         pass2(std::integral_constant<int, 0>{});
+      ATRACE(tr, 2, t, j);
+      pp_pass(j);
       tmem_st_wait();
       l = l * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
                       ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
@@ -633,6 +734,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
       tc_fence_before();  // P and the rescaled O (tcgen05.st) before the MMA issuer's PV_t(j)
       __syncwarp();
       if (lane == 0) mbar_arrive(bPReady + 8 * t);
+      ATRACE(tr, 3, t, j);
     }
     // ---------------------------------------------------------------- epilogue: O / l, lse
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
@@ -1554,6 +1656,12 @@ bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t b
 
 }  // namespace cy_attn
 
+#ifdef CY_ATTN_TRACE
+extern "C" int cy_attn_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, cy_attn::g_attn_trace, sizeof(cy_attn::g_attn_trace));
+}
+#endif
+
 extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t heads, int64_t seq_q, int64_t seq_k,
                                         int64_t head_dim, float scale, int causal, const void* Q, const void* K,
                                         const void* V, void* O, float* lse, void* stream) {
@@ -1678,7 +1786,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   const bool ps = kern == 1 && cs == 3 && emu == 0 && persist && seq_k > 0;
   const int ki = ps ? 6 : kern == 1 ? (cs == 2 ? 4 : cs == 3 ? 5 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
   const void* fn = fns[ki][dt][ps ? 0 : ei];
-  const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : SMEM_BYTES;
+  const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : (kern == 1 && cs == 3) ? SMEM_BYTES3 : SMEM_BYTES;
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     if (!g_attr_set[dev][ki][dt][ei]) {
