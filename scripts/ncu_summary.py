@@ -7,7 +7,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second",
         "lts__t_sector_hit_rate.pct", "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
-        "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "sm__ops_path_tensor_src_fp16_dst_fp32.sum"]
+        "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "sm__ops_path_tensor_src_fp16_dst_fp32.sum",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
 out = {}
 for arg in sys.argv[1:]:
     name, path = arg.split("=", 1)
