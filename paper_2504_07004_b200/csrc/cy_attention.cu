@@ -1149,9 +1149,8 @@ constexpr int V_BYTES = 128 * 128;              // 128 keys x this CTA's 64 colu
 constexpr int OFF_Q = 0, OFF_K = Q_BYTES, OFF_V = OFF_K + KS * K_BYTES, OFF_BAR = OFF_V + VS * V_BYTES;
 constexpr int OFF_X = OFF_BAR + 512;            // row-max exchange [2 parities][4 parts][128], l [4][128]
 constexpr int SMEM_BYTES = 1024 + OFF_X + (2 * 4 * 128 + 4 * 128) * 4;
-// NS = number of softmax warps sharing one row (column split): 2 (64 columns each) or 4 (32 each);
-// NS = 1: two groups of 4 warps that take alternate key blocks, each thread owning a whole row.
-template <int NS> __host__ __device__ constexpr int softmax_warps() { return NS == 1 ? 8 : 4 * NS; }
+// NS = number of softmax warps sharing one row (column split): 2 (64 columns each) or 4 (32 each).
+template <int NS> __host__ __device__ constexpr int softmax_warps() { return 4 * NS; }
 template <int NS> __host__ __device__ constexpr int threads() { return (softmax_warps<NS>() + 2) * 32; }
 constexpr uint32_t T_S = 0, T_O = 256, T_P = 384;
 
@@ -1179,9 +1178,9 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
   using namespace pr;
   constexpr int SW = softmax_warps<NS>();
   constexpr int W_PROD = SW, W_MMA = SW + 1;
-  constexpr bool ALT = (NS == 1);
-  constexpr int COLS = ALT ? 64 : 128 / NS;  // score / output columns per softmax thread (ALT: per pass)
-  constexpr int PER_BLOCK = ALT ? 4 : SW;    // softmax warps per CTA that read each S block
+  static_assert(NS == 2 || NS == 4, "row split into 2 or 4 column parts");
+  constexpr int COLS = 128 / NS;  // score / output columns per softmax thread
+  constexpr int PER_BLOCK = SW;   // softmax warps per CTA that read each S block
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -1189,9 +1188,8 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
   const uint32_t bar = base + OFF_BAR;
   const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bKFull + 8 * KS, bVFull = bKEmpty + 8 * KS,
                  bVEmpty = bVFull + 8 * VS, bSFull = bVEmpty + 8 * VS, bSFree = bSFull + 16, bPFull = bSFree + 16,
-                 bPVDone = bPFull + 8, bM = bPVDone + 16, sTmemSlot = bM + 16;
-  // bPVDone[2]: PV(j) completion, by parity of j (ALT: each group waits for the other group's PV
-  // without a two-phase ambiguity); bM[2] (ALT): group g posted the running max of its block
+                 bPVDone = bPFull + 8, sTmemSlot = bPVDone + 32;
+  // bPVDone[2]: PV(j) completion, by parity of j
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1221,7 +1219,6 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
       mbar_init(bSFull + 8 * b, 1);
       mbar_init(bSFree + 8 * b, 2 * PER_BLOCK);  // the softmax warps of both CTAs that read S
       mbar_init(bPVDone + 8 * b, 1);
-      mbar_init(bM + 8 * b, 4);
     }
     mbar_init(bPFull, 2 * PER_BLOCK);
     fence_mbar_init();
@@ -1306,176 +1303,6 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
         issue_pv(j);
       }
     }
-  } else if constexpr (ALT) {
-    // ---------------------------------------------------------------- softmax, alternating groups
-    // Group g (warps 4g..4g+3) handles key blocks j = g, g+2, ... (S buffer g), each thread a whole
-    // row in two 64-column passes, so one group's exponentials overlap the other group's TMEM
-    // loads, maxima and barrier waits.  The running max is handed from block to block through
-    // shared memory (bM[g]); each group keeps its row sum relative to the max it last used and
-    // the two sums are combined at the end (lse, O/l).
-    const int g = warp >> 2;
-    const int q = warp & 3;
-    const int r = 32 * q + lane;
-    const int qrow = trow0 + r;
-    const uint32_t lane_base = uint32_t(32 * q) << 16;
-    const uint32_t tS = tmem + lane_base + T_S + 128 * g;
-    const uint32_t tO = tmem + lane_base + T_O;
-    const uint32_t tP = tmem + lane_base + T_P;
-    float* mpost = reinterpret_cast<float*>(smem_raw + (base + OFF_X - raw));  // [2][BQ]
-    float* fin = mpost + 2 * BQ;                                                 // [2][2][BQ]: m, l
-    const uint32_t sfree_leader = mapa(bSFree + 8 * g, 0), pfull_leader = mapa(bPFull, 0);
-    float m = -INFINITY, l = 0.f;  // this group's row-sum reference max and row sum
-    int it = 0;
-    for (int j = g; j < n; j += 2, ++it) {
-      mbar_wait(bSFull + 8 * g, it & 1);
-      tc_fence_after();
-      const int key0 = j * BKV;
-      const bool full_block = (key0 + BKV <= p.sk) && (!p.causal || key0 + BKV - 1 <= trow0);
-      auto fix = [&](uint32_t (&v)[64], int c) {
-        if (!full_block) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e) {
-            const int key = key0 + 64 * c + e;
-            if (key >= p.sk || (p.causal && key > qrow)) v[e] = __float_as_uint(-INFINITY);
-          }
-        }
-      };
-      auto load64 = [&](uint32_t (&v)[64], int c) {
-        tmem_ld_32x32b_x32(tS + 64 * c, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-        tmem_ld_32x32b_x32(tS + 64 * c + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-        tmem_ld_wait();
-      };
-      float mx8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[64];
-        load64(v, c);
-        fix(v, c);
-#pragma unroll
-        for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
-      }
-      float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;
-      // the running max after block j-1 (posted by the other group), lazy rescaling as elsewhere
-      float mprev = -INFINITY;
-      if (j > 0) {
-        mbar_wait(bM + 8 * (g ^ 1), ((j - 1) >> 1) & 1);
-        mprev = mpost[(g ^ 1) * BQ + r];
-      }
-      float m_new = mprev, corr_o = 1.f;
-      if (mb > mprev + 8.f) {
-        m_new = mb;
-        corr_o = ex2(mprev - m_new);  // 0 when mprev == -inf
-      }
-      mpost[g * BQ + r] = m_new;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bM + 8 * g);
-      const float corr_l = (m == m_new) ? 1.f : ex2(m - m_new);  // this group's sum -> new reference
-      const float msub = (m_new == -INFINITY) ? 0.f : m_new;
-      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-      const float2 ms2 = make_float2(-msub, -msub);
-      float2 sm4[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[64];
-        load64(v, c);
-        if (c == 1) {  // S(j) is in registers: the tensor core may overwrite buffer g with S(j+2)
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(sfree_leader);
-        }
-        fix(v, c);
-        uint32_t pk[32];
-        auto exps = [&](auto e_c) {
-          constexpr int E = decltype(e_c)::value;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float2 x = ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sc2, ms2);
-            float2 pe;
-            if ((e & 7) < E) {
-              pe = ex2_emu2(x);
-            } else {
-              pe.x = ex2(x.x);
-              pe.y = ex2(x.y);
-            }
-            sm4[e & 3] = fadd2(sm4[e & 3], pe);
-            pk[e] = pack2<DT>(pe.x, pe.y);
-          }
-        };
-        if (EMU > 0 && full_block)
-          exps(std::integral_constant<int, EMU>{});
-        else
-          exps(std::integral_constant<int, 0>{});
-        if (c == 0 && j > 0) {  // PV(j-1) done: P is free and O holds P(0..j-1) V at max mprev
-          mbar_wait(bPVDone + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1);
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, corr_o != 1.f)) {
-#pragma unroll 1
-            for (int cc = 0; cc < 4; ++cc) {
-              uint32_t o[32];
-              tmem_ld_32x32b_x32(tO + 32 * cc, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr_o);
-              tmem_st_32x32b_x32(tO + 32 * cc, o);
-            }
-          }
-        }
-        tmem_st_32x32b_x32(tP + 32 * c, pk);
-      }
-      tmem_st_wait();
-      l = l * corr_l + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
-                        ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
-      m = m_new;
-      tc_fence_before();  // P and the rescaled O before the leader's PV(j)
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(pfull_leader);
-    }
-    // ---------------------------------------------------------------- epilogue: combine, O / l, lse
-    fin[(0 * 2 + g) * BQ + r] = m;
-    fin[(1 * 2 + g) * BQ + r] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // warps q and q + 4
-    const float m0 = fin[r], m1 = fin[BQ + r];
-    const float mf = fmaxf(m0, m1);  // the max after the last block (the running max only grows)
-    float lt = 0.f;
-    if (mf != -INFINITY) lt = fin[2 * BQ + r] * ex2(m0 - mf) + fin[3 * BQ + r] * ex2(m1 - mf);
-    const float inv_l = (lt > 0.f) ? 1.f / lt : 0.f;
-    if (n > 0) {
-      mbar_wait(bPVDone + 8 * ((n - 1) & 1), ((n - 1) >> 1) & 1);
-      tc_fence_after();
-    }
-    const uint32_t sE = sQ + (g * 4 + q) * 4096;  // 32 rows x 64 columns (SW128) per warp
-    uint32_t a[64];
-    if (n > 0) {
-      tmem_ld_32x32b_x32(tO + 64 * g, *reinterpret_cast<uint32_t(*)[32]>(&a[0]));
-      tmem_ld_32x32b_x32(tO + 64 * g + 32, *reinterpret_cast<uint32_t(*)[32]>(&a[32]));
-      tmem_ld_wait();
-    } else {
-#pragma unroll
-      for (int e = 0; e < 64; ++e) a[e] = 0u;
-    }
-#pragma unroll
-    for (int vv = 0; vv < 8; ++vv) {
-      uint32_t w[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        w[u] = pack2<DT>(__uint_as_float(a[8 * vv + 2 * u]) * inv_l, __uint_as_float(a[8 * vv + 2 * u + 1]) * inv_l);
-      st_shared_v4(sE + lane * 128 + ((vv ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_3d(&tmO, sE, 64 * g, trow0 + 32 * q, hb);
-      bulk_commit();
-    }
-    if (g == 0 && p.lse && qrow < p.sq)
-      p.lse[(size_t)hb * p.sq + qrow] = (lt > 0.f) ? (mf + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
-    if (lane == 0) bulk_wait_read<0>();
   } else {
     // ---------------------------------------------------------------- softmax / epilogue
     const int h = warp >> 2;        // column part (of NS)
@@ -1639,7 +1466,7 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_attr_mu;
-bool g_attr_set[64][7][2][4] = {};
+bool g_attr_set[64][6][2][4] = {};
 int g_sms[64] = {};
 
 bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r,
@@ -1709,7 +1536,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   const int split = [] {
     const char* e = std::getenv("CY_ATTN_SPLIT");
     const int v = e ? std::atoi(e) : 2;
-    return (v == 1 || v == 4) ? v : 2;
+    return v == 4 ? 4 : 2;
   }();
   CUtensorMap tQ, tK, tV, tO;
   std::memset(&tK, 0, sizeof(tK));
@@ -1740,7 +1567,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     const int v = e ? std::atoi(e) : 0;
     return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 0;
   }();
-  const void* fns[7][2][4] = {
+  const void* fns[6][2][4] = {
       {{(const void*)&attn_fwd_kernel<0, 0>, (const void*)&attn_fwd_kernel<0, 2>,
         (const void*)&attn_fwd_kernel<0, 3>, (const void*)&attn_fwd_kernel<0, 4>},
        {(const void*)&attn_fwd_kernel<1, 0>, (const void*)&attn_fwd_kernel<1, 2>,
@@ -1753,10 +1580,6 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
         (const void*)&attn_pair_kernel<0, 3, 4>, (const void*)&attn_pair_kernel<0, 4, 4>},
        {(const void*)&attn_pair_kernel<1, 0, 4>, (const void*)&attn_pair_kernel<1, 2, 4>,
         (const void*)&attn_pair_kernel<1, 3, 4>, (const void*)&attn_pair_kernel<1, 4, 4>}},
-      {{(const void*)&attn_pair_kernel<0, 0, 1>, (const void*)&attn_pair_kernel<0, 2, 1>,
-        (const void*)&attn_pair_kernel<0, 3, 1>, (const void*)&attn_pair_kernel<0, 4, 1>},
-       {(const void*)&attn_pair_kernel<1, 0, 1>, (const void*)&attn_pair_kernel<1, 2, 1>,
-        (const void*)&attn_pair_kernel<1, 3, 1>, (const void*)&attn_pair_kernel<1, 4, 1>}},
       {{(const void*)&attn_fwd_kernel<0, 0, 2>, (const void*)&attn_fwd_kernel<0, 2, 2>,
         (const void*)&attn_fwd_kernel<0, 3, 2>, (const void*)&attn_fwd_kernel<0, 4, 2>},
        {(const void*)&attn_fwd_kernel<1, 0, 2>, (const void*)&attn_fwd_kernel<1, 2, 2>,
@@ -1784,7 +1607,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     return e ? std::atoi(e) : 0;
   }();
   const bool ps = kern == 1 && cs == 3 && emu == 0 && persist && seq_k > 0;
-  const int ki = ps ? 6 : kern == 1 ? (cs == 2 ? 4 : cs == 3 ? 5 : 0) : (split == 2 ? 1 : split == 4 ? 2 : 3);
+  const int ki = ps ? 5 : kern == 1 ? (cs == 2 ? 3 : cs == 3 ? 4 : 0) : (split == 2 ? 1 : 2);
   const void* fn = fns[ki][dt][ps ? 0 : ei];
   const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : (kern == 1 && cs == 3) ? SMEM_BYTES3 : SMEM_BYTES;
   {
@@ -1805,7 +1628,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   if (kern == 2) {
     cfg.gridDim = dim3((unsigned)(2 * ((seq_q + 2 * BQ - 1) / (2 * BQ))), (unsigned)bh, 1);
-    cfg.blockDim = dim3(split == 2 ? pr::threads<2>() : split == 4 ? pr::threads<4>() : pr::threads<1>(), 1, 1);
+    cfg.blockDim = dim3(split == 2 ? pr::threads<2>() : pr::threads<4>(), 1, 1);
     attrs[1].id = cudaLaunchAttributeClusterDimension;
     attrs[1].val.clusterDim.x = 2;
     attrs[1].val.clusterDim.y = 1;

@@ -619,7 +619,7 @@ def test_attention_closed_forms():
 
 
 @pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("1", "2", "3"), ("1", "2", "3", "1"), ("2", "2", "1"),
-                                     ("2", "4", "1"), ("2", "1", "1")])
+                                     ("2", "4", "1")])
 @pytest.mark.parametrize("shape,causal", [((1, 2, 300, 500), False), ((2, 1, 640, 640), True), ((1, 3, 129, 257), False),
                                           ((1, 1, 1, 1), False), ((1, 2, 1024, 1024), True)])
 def test_attention_kernel_variants(variant, shape, causal, monkeypatch):
@@ -634,7 +634,7 @@ def test_attention_kernel_variants(variant, shape, causal, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", [("1", "2", "1"), ("1", "2", "2"), ("1", "2", "3"), ("1", "2", "3", "1"), ("2", "2", "1"),
-                                     ("2", "4", "1"), ("2", "1", "1")])
+                                     ("2", "4", "1")])
 def test_attention_kernel_variants_bf16_causal_ragged(variant, monkeypatch):
     monkeypatch.setenv("CY_ATTN_KERNEL", variant[0])
     monkeypatch.setenv("CY_ATTN_SPLIT", variant[1])
