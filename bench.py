@@ -149,6 +149,9 @@ def make_workload(name, rank, world, device):
 
     import paper_2504_07004_b200 as cy
     import synth
+    from paper_2504_07004_b200.stream import HostGemmPipeline, HostPipeline
+
+    f16 = torch.float16
 
     def up(bits):
         return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.float16).to(device)
@@ -204,12 +207,18 @@ def make_workload(name, rank, world, device):
         hD = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
         pipe = None
         if name == "gemm" or name.startswith("sweep-"):
-            from paper_2504_07004_b200.stream import HostGemmPipeline
-
             pipe = HostGemmPipeline(m_rank, n, k, device=device)
+        elif name == "rowreduce":
+            pipe = HostPipeline([((m_rank, k), f16), ((k, n), f16)], [((m_rank, n), f16), ((m_rank,), torch.float32)],
+                                lambda i, o, st: cy.gemm_rowreduce(i[0], i[1], out=o[0], y=o[1], stream=st),
+                                device=device)
+            hy = torch.empty((m_rank,), dtype=torch.float32).pin_memory()
 
         def e2e_step(i):
             j = i % nsets
+            if pipe is not None and name == "rowreduce":
+                pipe.submit((hA[j], hB[j]), (hD, hy))
+                return
             if pipe is not None:  # public host-streaming API: H2D / kernel / D2H overlapped
                 pipe.submit(hA[j], hB[j], hD)
                 return
@@ -223,7 +232,7 @@ def make_workload(name, rank, world, device):
         W["pipe"] = pipe
 
         W.update(flops=flops, step=step, e2e_step=e2e_step, desc=desc,
-                 h2d=hA[0].numel() * 2 + hB[0].numel() * 2, d2h=hD.numel() * 2,
+                 h2d=hA[0].numel() * 2 + hB[0].numel() * 2, d2h=hD.numel() * 2 + (4 * m_rank if name == "rowreduce" else 0),
                  shape={"m": m_rank * world, "n": n, "k": k, "m_per_gpu": m_rank},
                  oracle_case=("gemm", host_sets[0]), kernel_flops=flops)
     elif name == "batched":
@@ -242,9 +251,12 @@ def make_workload(name, rank, world, device):
         hA, hB = pinned(A), pinned(B)
         hD = torch.empty((L, m, m), dtype=torch.float16).pin_memory()
 
+        pipe = HostPipeline([((L, m, m), f16), ((L, m, m), f16)], [((L, m, m), f16)],
+                            lambda i, o, st: cy.gemm_batched(i[0], i[1], out=o[0], stream=st), device=device)
+
         def e2e_step(i):
-            cy.gemm_batched(hA.to(device, non_blocking=True), hB.to(device, non_blocking=True), out=D)
-            hD.copy_(D, non_blocking=True)
+            pipe.submit((hA, hB), (hD,))
+        W["pipe"] = pipe
         W.update(flops=2.0 * L * m ** 3, step=step, e2e_step=e2e_step,
                  desc=f"batched fp16 GEMM 64 x 1024^3 (configs[2]), batch-sharded over {world} GPU(s)",
                  h2d=2 * hA.numel() * 2, d2h=hD.numel() * 2, shape={"batch": L_total, "m": m, "n": m, "k": m},
@@ -263,10 +275,13 @@ def make_workload(name, rank, world, device):
         hA, hB0, hB1 = pinned(A), pinned(B0), pinned(B1)
         hD0 = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
 
+        pipe = HostPipeline([((m_rank, n), f16), ((n, n), f16), ((n, n), f16)], [((m_rank, n), f16)],
+                            lambda i, o, st: cy.dual_gemm_glu(i[0], i[1], i[2], act="silu", out=o[0], stream=st),
+                            device=device)
+
         def e2e_step(i):
-            cy.dual_gemm_glu(hA.to(device, non_blocking=True), hB0.to(device, non_blocking=True),
-                             hB1.to(device, non_blocking=True), act="silu", out=D0)
-            hD0.copy_(D0, non_blocking=True)
+            pipe.submit((hA, hB0, hB1), (hD0,))
+        W["pipe"] = pipe
         W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
                  desc="GLU dual-GEMM D = silu(A*B0) * (A*B1), 8192^3 (SURVEY NEXT-3, P:1532)",
                  h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=hD0.numel() * 2,
@@ -288,11 +303,13 @@ def make_workload(name, rank, world, device):
         hD0 = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
         hD1 = torch.empty_like(hD0).pin_memory()
 
+        pipe = HostPipeline([((m_rank, n), f16), ((n, n), f16), ((n, n), f16)], [((m_rank, n), f16)] * 2,
+                            lambda i, o, st: cy.dual_gemm(i[0], i[1], i[2], mode="pair", out0=o[0], out1=o[1],
+                                                          stream=st), device=device)
+
         def e2e_step(i):
-            cy.dual_gemm(hA.to(device, non_blocking=True), hB0.to(device, non_blocking=True),
-                         hB1.to(device, non_blocking=True), mode="pair", out0=D0, out1=D1)
-            hD0.copy_(D0, non_blocking=True)
-            hD1.copy_(D1, non_blocking=True)
+            pipe.submit((hA, hB0, hB1), (hD0, hD1))
+        W["pipe"] = pipe
         W.update(flops=4.0 * m_rank * n * n, step=step, e2e_step=e2e_step,
                  desc=f"dual-GEMM D=(A*B0, A*B1), 8192^3 (configs[3])" + (f", M-sharded over {world}" if world > 1 else ""),
                  h2d=(hA.numel() + hB0.numel() + hB1.numel()) * 2, d2h=2 * hD0.numel() * 2,
@@ -316,10 +333,13 @@ def make_workload(name, rank, world, device):
         hQ, hK, hV = (pinned(x).view(b, h, s_len, d) for x in host[0])
         hO = torch.empty((b, h, s_len, d), dtype=torch.float16).pin_memory()
 
+        qkv = ((b, h, s_len, d), f16)
+        pipe = HostPipeline([qkv] * 3, [qkv], lambda i, o, st: cy.attention(i[0], i[1], i[2], out=o[0], lse=lse,
+                                                                          stream=st), device=device)
+
         def e2e_step(i):
-            cy.attention(hQ.to(device, non_blocking=True), hK.to(device, non_blocking=True),
-                         hV.to(device, non_blocking=True), out=O, lse=lse)
-            hO.copy_(O, non_blocking=True)
+            pipe.submit((hQ, hK, hV), (hO,))
+        W["pipe"] = pipe
         fl = 4.0 * b * h * s_len * s_len * d
         W.update(flops=fl, step=step, e2e_step=e2e_step,
                  desc=f"FA forward fp16 HeadDim 128, non-causal, batch {b} x 16 heads x 8192 (P:1594-1636, SURVEY NEXT-4)"
@@ -559,7 +579,7 @@ def main():
         e_total = maxred(e_total)
         e2e = {"value": W["flops"] * world / (e_total / e_steps * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(W["h2d"]), "d2h_bytes_per_step": int(W["d2h"]),
-               "ms_per_step": e_total / e_steps, "path": ("HostGemmPipeline: pinned H2D, C-ABI kernel and D2H on three streams, overlapped across steps"
+               "ms_per_step": e_total / e_steps, "path": (f"{type(W['pipe']).__name__}: pinned H2D, C-ABI call and D2H on three streams, overlapped across steps"
                         if W.get("pipe") is not None else "pinned host -> device copies + C-ABI call + D -> pinned host")}
 
     cpu = None

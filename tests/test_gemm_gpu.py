@@ -471,6 +471,46 @@ def test_host_pipeline_overlapped_steps():
                           oracle.encode("f16", oracle.gemm("f16", A, B)), "pipeline step")
 
 
+def test_generic_host_pipeline_rowreduce_and_batched():
+    """paper_2504_07004_b200.stream.HostPipeline (the bench's end-to-end path for every workload):
+    overlapped steps of the row-reduce GEMM (two outputs, D and fp32 y) and of the batched GEMM give
+    the oracle's exact results on integer inputs."""
+    from paper_2504_07004_b200.stream import HostPipeline
+
+    def pinned(x):
+        return torch.from_numpy(x.view(np.int16)).view(torch.float16).pin_memory()
+
+    m, n, k, steps = 384, 264, 320, 4
+    f16 = torch.float16
+    pipe = HostPipeline([((m, k), f16), ((k, n), f16)], [((m, n), f16), ((m,), torch.float32)],
+                        lambda i, o, st: cy.gemm_rowreduce(i[0], i[1], out=o[0], y=o[1], stream=st))
+    ins, outs = [], []
+    for s_ in range(steps):
+        A, B, _ = synth.gemm_inputs(m, n, k, seed=301 + s_, kind="int")
+        hD = torch.empty((m, n), dtype=f16).pin_memory()
+        hy = torch.empty((m,), dtype=torch.float32).pin_memory()
+        ins.append((A, B))
+        outs.append((hD, hy))
+        pipe.submit((pinned(A), pinned(B)), (hD, hy))
+    pipe.synchronize()
+    for (A, B), (hD, hy) in zip(ins, outs):
+        assert_bits_equal(hD.view(torch.int16).numpy().view(np.uint16),
+                          oracle.encode("f16", oracle.gemm("f16", A, B)), "pipeline D")
+        assert np.array_equal(hy.numpy().astype(np.float64), oracle.rowsum("f16", A))
+
+    L, mb = 3, 136
+    pipe = HostPipeline([((L, mb, mb), f16)] * 2, [((L, mb, mb), f16)],
+                        lambda i, o, st: cy.gemm_batched(i[0], i[1], out=o[0], stream=st))
+    for s_ in range(2):
+        As, Bs = zip(*[synth.gemm_inputs(mb, mb, mb, seed=401 + 10 * s_ + b, kind="int")[:2] for b in range(L)])
+        hD = torch.empty((L, mb, mb), dtype=f16).pin_memory()
+        pipe.submit((pinned(np.stack(As)), pinned(np.stack(Bs))), (hD,))
+        pipe.synchronize()
+        for b in range(L):
+            assert_bits_equal(hD[b].view(torch.int16).numpy().view(np.uint16),
+                              oracle.encode("f16", oracle.gemm("f16", As[b], Bs[b])), "pipeline batched")
+
+
 # ---------------------------------------------------------------- SURVEY section 4 coverage
 EDGE = [1, 7, 63, 64, 65, 127, 129, 255, 257, 1000, 1023]
 _rng = np.random.default_rng(20250407)
