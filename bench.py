@@ -34,6 +34,16 @@ METRIC = "fp16 GEMM TFLOP/s per B200 and % of dense tensor peak; 8-GPU aggregate
 ATTN_METRIC = "fp16 flash-attention forward TFLOP/s (HeadDim 128, 4*b*h*s^2*d FLOP)"
 
 
+def step_stats(per):
+    """Mean / p10 / median / p90 of the per-step device times (ms); with a single region
+    event pair (short steps) only the mean exists."""
+    out = {"mean": round(statistics.mean(per), 5), "n": len(per)}
+    if len(per) >= 10:
+        q = statistics.quantiles(per, n=10)
+        out.update(p10=round(q[0], 5), median=round(statistics.median(per), 5), p90=round(q[-1], 5))
+    return out
+
+
 def scaling_of(workload):
     """'weak' when every rank's work is fixed as N grows (gemm: 8192 rows per GPU; sweep-n: n rows per
     GPU; attention: batch 2 per GPU), 'strong' when the total problem is fixed and split over the
@@ -611,6 +621,7 @@ def main():
                          "kernel_ms": round(kern_ms, 5)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "step_ms": step_stats(per),
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
             "timing": "CUDA events on the launching stream; barrier+sync both sides; max over ranks"
