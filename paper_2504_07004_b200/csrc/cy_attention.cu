@@ -632,11 +632,22 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         }
         tmem_ld_wait();
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          fix(vrow[g], g);
+        for (int g = 0; g < 2; ++g) fix(vrow[g], g);
+        // balanced 3-ary tree (depth 5, every level independent ops) instead of 8 serial chains
+        auto sc = [&](int k) { return __uint_as_float(vrow[k >> 6][k & 63]); };
+        auto max3 = [](float a, float b, float c) { return fmaxf(fmaxf(a, b), c); };
+        float l1[43];
 #pragma unroll
-          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(vrow[g][e]));
-        }
+        for (int i = 0; i < 42; ++i) l1[i] = max3(sc(3 * i), sc(3 * i + 1), sc(3 * i + 2));
+        l1[42] = fmaxf(sc(126), sc(127));
+        float l2[15];
+#pragma unroll
+        for (int i = 0; i < 14; ++i) l2[i] = max3(l1[3 * i], l1[3 * i + 1], l1[3 * i + 2]);
+        l2[14] = l1[42];
+        float l3[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) l3[i] = max3(l2[3 * i], l2[3 * i + 1], l2[3 * i + 2]);
+        mx8[0] = max3(max3(l3[0], l3[1], l3[2]), l3[3], l3[4]);
       } else {
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
