@@ -658,18 +658,21 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
           for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
         }
       }
-      float mb = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      float mb = (CS == 3) ? mx8[0]  // (the tree above already reduced the whole row)
+                           : fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mb = (mb == -INFINITY) ? -INFINITY : mb * p.scale_log2;  // scale_log2 > 0 keeps the order
       // Lazy rescaling: keep the running max unless it grows by more than 2^8 (P <= 256 stays exact
       // in the 16-bit types and the fp32 sums); the final O / l uses the same max, so this is exact.
+      // The vote reads the comparison, not corr, so it does not wait for the SFU.
+      const bool grow = mb > m + 8.f;
       float m_new = m, corr = 1.f;
-      if (mb > m + 8.f) {
+      if (grow) {
         m_new = mb;
         corr = ex2(m - m_new);  // 0 when m == -inf
       }
       const float msub = (m_new == -INFINITY) ? 0.f : m_new;
-      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {  // O_t holds PV_t(j-1) (waited above)
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O_t holds PV_t(j-1) (waited above)
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
