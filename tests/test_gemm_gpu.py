@@ -731,3 +731,34 @@ def test_attention_large_sampled():
     got = decode(to_bits(O).reshape(b * h, s, 128)[:, rows], "f16")
     tol = 2 * 2.0 ** -11 * np.abs(decode(V, "f16")).max() + 3 * 2.0 ** -11 * np.abs(Oref) + 1e-6
     assert (np.abs(got - Oref) <= tol).all()
+
+
+# ---------------------------------------------------------------- bench.py contract (driver-facing)
+def test_bench_json_contract():
+    """One short default bench run prints one JSON line with every key the driver reads: the
+    headline metric and value, roofline (bound / achieved / peak / frac / traffic), cpu_baseline
+    (the oracle), e2e with the copied bytes, clocks, and one kernel launch per timed step."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["steps"] == 5 and d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 5
+    rl = d["roofline"]
+    assert rl["bound"] == "tensor" and rl["unit"] == "TFLOP/s" and 0 < rl["frac"] <= 1.2
+    assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 8192 * 8192 * 2 and e["d2h_bytes_per_step"] == 8192 * 8192 * 2
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
