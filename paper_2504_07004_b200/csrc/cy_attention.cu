@@ -3,19 +3,24 @@
 //
 //   S = scale * Q K^T,  P = softmax_rows(S) (causal: key j <= query i),  O = P V,  lse = log sum exp S
 //
-// attn_fwd_kernel (default): one CTA per (two 128-row query tiles, batch*head), 10 warps.
+// attn_fwd_kernel (default layout CS = 3): one CTA per (two 128-row query tiles, batch*head),
+// 12 warps (3 warpgroups; setmaxnreg moves registers to the softmax warpgroups).
 //   warps 0-3, 4-7  softmax warpgroups of query tiles 0 and 1 (thread = query row = TMEM lane): per
-//                   128-key block, pass 1 reads S_t from TMEM for the row max, pass 2 re-reads it,
-//                   computes P = exp2(s*scale*log2e - m) in the exp2 domain and writes P_t (16-bit
-//                   pairs) back over S_t; lazy rescale of O_t in TMEM only when the max grows by
-//                   more than 2^8; final O / l, TMA store, lse.
-//   warp 8          TMA producer: both Q tiles once, then K_j and V_j through two separate 2-slot
-//                   rings (each refilled as soon as its last reader is done).
+//                   128-key block, one TMEM pass reads the row's 128 scores into registers, the row
+//                   max is a balanced FMNMX3 tree, P = exp2(s*scale*log2e - m) in the exp2 domain is
+//                   written back over S_t as 16-bit pairs (the first half published early so PV can
+//                   start); lazy rescale of O_t in TMEM only when the max grows by more than 2^8;
+//                   final O / l, TMA store, lse.
+//   warp 8          TMA producer: both Q tiles once, then K_j (2-slot ring) and V_j (3-slot ring),
+//                   each slot refilled as soon as its last reader is done.
 //   warp 9          tcgen05.mma issuer, per block j and tile t: O_t += P_t V_j (A = P_t read from
-//                   TMEM), then S_t(j+1) = Q_t K_{j+1}^T.  While one warpgroup runs its softmax the
-//                   tensor core runs the other tile's two GEMMs -- the FA3 ping-pong
-//                   with TMEM in place of FA3's register copy of S; every K/V block serves 256 rows.
-//   TMEM: S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512).  Shared: Q 2 x 32 KB, K/V 2 x 64 KB.
+//                   TMEM, in two halves), then S_t(j+1) = Q_t K_{j+1}^T.  While one warpgroup runs its
+//                   softmax the tensor core runs the other tile's two GEMMs -- the FA3 ping-pong
+//                    with TMEM in place of FA3's register copy of S; every K/V block
+//                   serves 256 rows.  Warps 10-11 only donate registers.
+//   TMEM: S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512).  Shared: Q 2 x 32 KB, K 2 x 32 KB,
+//   V 3 x 32 KB.  CS = 1 (10 warps, two TMEM passes) and CS = 2 (two warps per row, both tiles in
+//   turn) are the earlier layouts, kept as tested variants.
 // attn_pair_kernel (CY_ATTN_KERNEL=2): a CTA pair issuing cta_group::2 MMAs with double-buffered
 //   S and a separate P in TMEM (see its own comment); correct, measured slower.
 #include <cuda.h>
