@@ -8,14 +8,21 @@ SURVEY.md section 8(a).  No collective is on the data path (weak scaling).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
 
-Other workloads (--workload): sweep-<n> (n^3), batched (64 x 1024^3, batch-sharded),
-dual (dual-GEMM pair 8192^3), glu (silu(A*B0)*(A*B1) 8192^3), rowreduce (65536/P x 8192 x
-8192 + y), allgather (rowreduce + NCCL all-gather of D and y, replicated result), attention
-(FA forward fp16, HeadDim 128, 2 x 16 heads x 8192, non-causal; batch-sharded).
+--gpus N > 1 without torchrun: the script re-launches itself under torch.distributed.run with N
+processes (one per GPU, NCCL); under torchrun it checks that WORLD_SIZE == N.
+
+Other workloads (--workload): sweep-<n> (n^3), batched (64 x 1024^3, batch-sharded; beta = 0),
+batched-beta1 (the same with D = A*B + C: the HBM-bound case of SURVEY 8(d)), dual (dual-GEMM
+pair 8192^3), glu (silu(A*B0)*(A*B1) 8192^3), rowreduce (65536/P x 8192 x 8192 + y), allgather
+(rowreduce + chunked point-to-point exchange of D and y overlapped with the compute: replicated
+result), allgather-fused (GEMM whose epilogue stores every tile into every rank's D over peer
+mappings, device barriers around it), attention (FA forward fp16, HeadDim 128, 2 x 16 heads x
+8192, non-causal; batch-sharded).
 
 Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream, W warm-up
 steps, barrier + synchronize on both sides of exactly K timed steps, max over ranks.
-L2: inputs rotate over two input sets whose total exceeds the 126 MB L2.
+L2: the JSON "l2" key states, per workload, how many input sets rotate and their total bytes
+(> 126 MB L2 except where it says "L2-resident").
 """
 from __future__ import annotations
 
@@ -48,7 +55,8 @@ def scaling_of(workload):
     """'weak' when every rank's work is fixed as N grows (gemm: 8192 rows per GPU; sweep-n: n rows per
     GPU; attention: batch 2 per GPU), 'strong' when the total problem is fixed and split over the
     ranks (batched 64 x 1024^3, rowreduce/allgather 65536 rows, dual/glu 8192^3)."""
-    return "strong" if workload in ("batched", "rowreduce", "allgather", "dual", "glu") else "weak"
+    return "strong" if workload in ("batched", "batched-beta1", "rowreduce", "allgather", "allgather-fused", "dual",
+                                    "glu") else "weak"
 
 
 def metric_for(workload):
@@ -159,6 +167,7 @@ def make_workload(name, rank, world, device):
 
     import paper_2504_07004_b200 as cy
     import synth
+    from paper_2504_07004_b200.dist import sharded_gemm, sharded_gemm_rowreduce
     from paper_2504_07004_b200.stream import HostGemmPipeline, HostPipeline
 
     f16 = torch.float16
@@ -171,7 +180,13 @@ def make_workload(name, rank, world, device):
         return t.pin_memory()
 
     W = {}
-    if name in ("gemm", "rowreduce", "allgather") or name.startswith("sweep-"):
+
+    def l2_label(nsets, set_bytes):
+        tot = nsets * set_bytes
+        return (f"{nsets} input set(s) rotating, {tot / 1e6:.0f} MB of operands "
+                + ("(> 126 MB L2: not L2-resident)" if tot > 126e6 else "(L2-resident)"))
+
+    if name in ("gemm", "rowreduce", "allgather", "allgather-fused") or name.startswith("sweep-"):
         if name.startswith("sweep-"):
             n = int(name.split("-")[1])
             m_rank, k = n, n
@@ -182,18 +197,28 @@ def make_workload(name, rank, world, device):
             m_rank = 8192
             desc = ("fp16 GEMM 8192^3 (configs[1] 8192 point)" if world == 1 else
                     f"fp16 GEMM {8192 * world} x 8192 x 8192 M-sharded over {world} GPUs (configs[4] shape, no reduction)")
+        elif name == "allgather-fused":
+            n = k = 8192
+            m_rank = 65536 // world
+            desc = (f"fp16 GEMM 65536 x 8192 x 8192 M-sharded over {world} GPU(s), replicated D by fused replication "
+                     "(epilogue stores every tile into every rank's D over peer mappings; SURVEY NEXT-2)")
         else:
             n = k = 8192
             m_rank = 65536 // world
             desc = (f"fp16 GEMM 65536 x 8192 x 8192 + fused row reduction y(i)=sum_k A(i,k) (configs[4]), "
-                    f"M-sharded over {world} GPU(s)" + (", NCCL all-gather of D and y (replicated)" if name == "allgather" else ""))
+                    f"M-sharded over {world} GPU(s)" + (", D and y exchanged (chunked NCCL point-to-point overlapped "
+                                                        "with the compute; replicated result)" if name == "allgather" else ""))
         sets = []
         host_sets = []
-        nsets = 2 if m_rank * k * 2 + k * n * 2 < 400e6 else 1
+        set_bytes = m_rank * k * 2 + k * n * 2
+        # enough rotating sets that the operands exceed 2x the 126 MB L2 (one set when a set is > 400 MB)
+        nsets = 1 if set_bytes >= 400e6 else min(64, max(2, -(-int(300e6) // set_bytes)))
+        W["l2"] = l2_label(nsets, set_bytes)
         for s in range(nsets):
             A = synth.uniform((m_rank, k), synth.seed_for(4 if name in ("rowreduce", "allgather") else 1, 10 * rank + s))
             B = synth.uniform((k, n), synth.seed_for(1, 1000 + s))  # replicated across ranks
-            host_sets.append((A, B))
+            if s < 2:
+                host_sets.append((A, B))
             sets.append((up(A), up(B)))
         D = torch.empty((m_rank, n), dtype=torch.float16, device=device)
         y = torch.empty((m_rank,), dtype=torch.float32, device=device)
@@ -206,12 +231,21 @@ def make_workload(name, rank, world, device):
             def step(i):
                 a, b = sets[i % nsets]
                 cy.gemm_rowreduce(a, b, out=D, y=y)
+        elif name == "allgather-fused":
+            def step(i):
+                a, b = sets[i % nsets]
+                sharded_gemm(a, b, m_total=m_rank * world, replicate="fused")
         else:
-            from paper_2504_07004_b200.dist import sharded_gemm_rowreduce
-
             def step(i):
                 a, b = sets[i % nsets]
                 sharded_gemm_rowreduce(a, b, m_total=m_rank * world, replicate=True)
+        if name in ("allgather", "allgather-fused"):
+            # the exchange's physical bound: every rank receives (P-1)/P of D (and y)
+            # over NVLink; measured peer copy 770 GB/s per direction (B200_PROFILING.md)
+            recv = (world - 1) / world * (65536 * n * 2 + (65536 * 4 if name == "allgather" else 0))
+            W["exchange"] = {"recv_bytes_per_rank": int(recv), "nvlink_gbs": 770.0,
+                             "nvlink_bound_ms": round(recv / 770e9 * 1e3, 4),
+                             "compute_ms_at_peak": None}
         hA = [pinned(h[0]) for h in host_sets]
         hB = [pinned(h[1]) for h in host_sets]
         hD = torch.empty((m_rank, n), dtype=torch.float16).pin_memory()
@@ -234,30 +268,45 @@ def make_workload(name, rank, world, device):
                 return
             a = hA[j].to(device, non_blocking=True)
             b = hB[j].to(device, non_blocking=True)
-            if name in ("rowreduce", "allgather"):
-                cy.gemm_rowreduce(a, b, out=D, y=y)
+            if name == "allgather":  # the same replicated call, full D and y back to the host
+                Df, yf = sharded_gemm_rowreduce(a, b, m_total=m_rank * world, replicate=True)
+                hDf.copy_(Df, non_blocking=True)
+                hyf.copy_(yf, non_blocking=True)
+            elif name == "allgather-fused":
+                hDf.copy_(sharded_gemm(a, b, m_total=m_rank * world, replicate="fused"), non_blocking=True)
             else:
                 cy.gemm(a, b, out=D)
-            hD.copy_(D, non_blocking=True)
+                hD.copy_(D, non_blocking=True)
+        d2h = hD.numel() * 2 + (4 * m_rank if name == "rowreduce" else 0)
+        if name in ("allgather", "allgather-fused"):
+            hDf = torch.empty((m_rank * world, n), dtype=torch.float16).pin_memory()
+            hyf = torch.empty((m_rank * world,), dtype=torch.float32).pin_memory()
+            d2h = hDf.numel() * 2 + (hyf.numel() * 4 if name == "allgather" else 0)
         W["pipe"] = pipe
 
         W.update(flops=flops, step=step, e2e_step=e2e_step, desc=desc,
-                 h2d=hA[0].numel() * 2 + hB[0].numel() * 2, d2h=hD.numel() * 2 + (4 * m_rank if name == "rowreduce" else 0),
+                 h2d=hA[0].numel() * 2 + hB[0].numel() * 2, d2h=d2h,
                  shape={"m": m_rank * world, "n": n, "k": k, "m_per_gpu": m_rank},
-                 oracle_case=("gemm", host_sets[0]), kernel_flops=flops)
-    elif name == "batched":
+                 oracle_case=(("rowreduce" if name in ("rowreduce", "allgather") else "gemm"), host_sets[0]),
+                 kernel_flops=flops)
+    elif name in ("batched", "batched-beta1"):
         L_total, m = 64, 1024
         L = L_total // world
+        beta = 1.0 if name == "batched-beta1" else 0.0
         A = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank))
         B = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 1))
         A2 = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 2))
         B2 = synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 3))
         sets = [(up(A), up(B)), (up(A2), up(B2))]
+        Cs = [None, None]
+        if beta != 0:
+            Cs = [up(synth.uniform((L, m, m), synth.seed_for(2, 10 * rank + 4 + j))) for j in range(2)]
         D = torch.empty((L, m, m), dtype=torch.float16, device=device)
+        W["l2"] = l2_label(2, (2 + (beta != 0)) * L * m * m * 2)
 
         def step(i):
             a, b = sets[i % 2]
-            cy.gemm_batched(a, b, out=D)
+            cy.gemm_batched(a, b, Cs[i % 2], 1.0, beta, out=D)
         hA, hB = pinned(A), pinned(B)
         hD = torch.empty((L, m, m), dtype=torch.float16).pin_memory()
 
@@ -268,7 +317,8 @@ def make_workload(name, rank, world, device):
             pipe.submit((hA, hB), (hD,))
         W["pipe"] = pipe
         W.update(flops=2.0 * L * m ** 3, step=step, e2e_step=e2e_step,
-                 desc=f"batched fp16 GEMM 64 x 1024^3 (configs[2]), batch-sharded over {world} GPU(s)",
+                 desc=f"batched fp16 GEMM 64 x 1024^3 (configs[2]), batch-sharded over {world} GPU(s)"
+                      + (", D = A*B + C (beta = 1)" if beta != 0 else ""),
                  h2d=2 * hA.numel() * 2, d2h=hD.numel() * 2, shape={"batch": L_total, "m": m, "n": m, "k": m},
                  oracle_case=("batched", (A, B)), kernel_flops=2.0 * L * m ** 3)
     elif name == "glu":
@@ -279,6 +329,7 @@ def make_workload(name, rank, world, device):
         B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
         dA, dB0, dB1 = up(A), up(B0), up(B1)
         D0 = torch.empty((m_rank, n), dtype=torch.float16, device=device)
+        W["l2"] = l2_label(1, (m_rank * n + 2 * n * n) * 2)
 
         def step(i):
             cy.dual_gemm_glu(dA, dB0, dB1, act="silu", out=D0)
@@ -306,6 +357,7 @@ def make_workload(name, rank, world, device):
         dA, dB0, dB1 = up(A), up(B0), up(B1)
         D0 = torch.empty((m_rank, n), dtype=torch.float16, device=device)
         D1 = torch.empty_like(D0)
+        W["l2"] = l2_label(1, (m_rank * n + 2 * n * n) * 2)
 
         def step(i):
             cy.dual_gemm(dA, dB0, dB1, mode="pair", out0=D0, out1=D1)
@@ -336,6 +388,7 @@ def make_workload(name, rank, world, device):
             sets.append(tuple(up(x).view(b, h, s_len, d) for x in (Q, K, V)))
         O = torch.empty((b, h, s_len, d), dtype=torch.float16, device=device)
         lse = torch.empty((b, h, s_len), dtype=torch.float32, device=device)
+        W["l2"] = l2_label(2, 3 * b * h * s_len * d * 2)
 
         def step(i):
             q, k, v = sets[i % 2]
@@ -362,8 +415,57 @@ def make_workload(name, rank, world, device):
     return W
 
 
+def oracle_unit_fn(kind, arrs):
+    """The fp64 C oracle, as it stands, on a subset of the workload's output units: returns
+    (fn(units), FLOP per unit, number of units, unit name).  A unit is one output row (all columns,
+    full K) or, for the batched workload, one whole 1024^3 GEMM of the batch."""
+    import oracle
+
+    if kind == "batched":
+        A, B = arrs
+
+        def fn(units):
+            for r in units:
+                oracle.gemm("f16", A[r], B[r])
+        return fn, 2.0 * A.shape[1] * A.shape[2] * B.shape[2], A.shape[0], "whole 1024^3 GEMMs of the batch"
+    if kind == "dual":
+        A, B0, B1 = arrs
+        return (lambda rows: oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows), 4.0 * B0.shape[1] * A.shape[1],
+                A.shape[0], "rows (all columns, full K) of both products")
+    if kind == "glu":
+        A, B0, B1 = arrs
+        return (lambda rows: oracle.dual_glu("f16", "silu", A, B0, B1, rows=rows), 4.0 * B0.shape[1] * A.shape[1],
+                A.shape[0], "rows (all columns, full K)")
+    if kind == "rowreduce":
+        A, B = arrs
+
+        def fn(rows):
+            oracle.gemm("f16", A, B, rows=rows % A.shape[0])
+            oracle.rowsum("f16", A, rows=rows % A.shape[0])
+        return fn, 2.0 * B.shape[1] * A.shape[1] + A.shape[1], 65536, "rows (all columns, full K) + row sums"
+    A, B = arrs
+    return (lambda rows: oracle.gemm("f16", A, B, rows=rows), 2.0 * B.shape[1] * A.shape[1], A.shape[0],
+            "rows (all columns, full K)")
+
+
+def oracle_calibrate(fn, m, nth):
+    """t(units) = fixed (operand decode) + units * per_unit, from two probes."""
+    import numpy as np
+
+    p1 = max(1, min(m // 2, max(2 * nth, 8)))
+    t0 = time.perf_counter()
+    fn(np.arange(p1))
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fn(np.arange(min(m, 2 * p1)))
+    t2 = time.perf_counter() - t0
+    per = max((t2 - t1) / max(1, min(m, 2 * p1) - p1), 1e-6)
+    return max(t1 - per * p1, 0.0), per, p1
+
+
 def oracle_baseline(case, budget_s=12.0):
-    """Time the fp64 C oracle, as it stands, on a bounded row sample of the same workload."""
+    """Time the fp64 C oracle, as it stands, on a bounded sample of the same workload (one call
+    sized to ~budget_s of CPU work: >= 512 rows)."""
     import numpy as np
 
     import oracle
@@ -371,53 +473,18 @@ def oracle_baseline(case, budget_s=12.0):
     kind, arrs = case
     oracle.set_threads(len(os.sched_getaffinity(0)))
     nth = oracle.num_threads()
-    if kind == "batched":
-        A, B = arrs
-        L = A.shape[0]
-        t0 = time.perf_counter()
-        used = 0
-        for b in range(L):
-            oracle.gemm("f16", A[b], B[b])
-            used += 1
-            if time.perf_counter() - t0 > budget_s:
-                break
-        dt = time.perf_counter() - t0
-        m = A.shape[1]
-        flops = 2.0 * used * m ** 3
-        return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
-                "sample": f"{used} of {L} batches of 1024^3 (full GEMMs), fp64 C oracle, {dt:.1f} s"}
     if kind == "attention":
         return attention_sample(*arrs, budget_s=budget_s)
-    if kind == "dual":
-        A, B0, B1 = arrs
-        fn = lambda rows: oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows)  # noqa: E731
-        per_row = 4.0 * B0.shape[1] * A.shape[1]
-    elif kind == "glu":
-        A, B0, B1 = arrs
-        fn = lambda rows: oracle.dual_glu("f16", "silu", A, B0, B1, rows=rows)  # noqa: E731
-        per_row = 4.0 * B0.shape[1] * A.shape[1]
-    else:
-        A, B = arrs
-        fn = lambda rows: oracle.gemm("f16", A, B, rows=rows)  # noqa: E731
-        per_row = 2.0 * B.shape[1] * A.shape[1]
-    m = A.shape[0]
-    # calibrate: t(rows) = fixed (B decode) + rows * per_row_time, from two probes
-    p1 = max(2 * nth, 8)
+    fn, per_unit, m, unit = oracle_unit_fn(kind, arrs)
+    fixed, per, p1 = oracle_calibrate(fn, m, nth)
+    floor = 1 if kind == "batched" else min(m, 512)
+    nunits = int(min(m, max(floor, p1, (budget_s - fixed) / per)))
+    units = np.linspace(0, m - 1, nunits).astype(np.int64)
     t0 = time.perf_counter()
-    fn(np.arange(min(m, p1)))
-    t1 = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    fn(np.arange(min(m, 2 * p1)))
-    t2 = time.perf_counter() - t0
-    per = max((t2 - t1) / p1, 1e-6)
-    fixed = max(t1 - per * p1, 0.0)
-    nrows = int(min(m, max(p1, (budget_s - fixed) / per)))
-    rows = np.linspace(0, m - 1, nrows).astype(np.int64)
-    t0 = time.perf_counter()
-    fn(rows)
+    fn(units)
     dt = time.perf_counter() - t0
-    return {"value": per_row * nrows / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
-            "sample": f"{nrows} of {m} rows (all columns, full K) of the same inputs, fp64 C oracle, {dt:.1f} s"}
+    return {"value": per_unit * nunits / dt / 1e12, "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
+            "sample": f"{nunits} of {m} {unit} of the same inputs, fp64 C oracle, {dt:.1f} s"}
 
 
 def attention_sample(Q, K, V, bh, budget_s=12.0, rng=None):
@@ -464,7 +531,19 @@ def main():
                     help="capture the K timed steps in a CUDA graph and time its replay (no host launch gaps)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's launch form)
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one process per GPU")
 
     if args.impl == "reference":
         return reference_arm(args, rank, world)
@@ -578,9 +657,10 @@ def main():
     value = W["flops"] * world / (ms_per_step * 1e-3) / 1e12
     peaks = load_peaks()
     achieved = W["kernel_flops"] / (kern_ms * 1e-3) / 1e12
-    # burst figure for a short timed region, the sustained (power-capped) one for >= 0.5 s
-    long_region = total_ms >= 500.0
-    peak = peaks["sustained"] if long_region else peaks["burst"]
+    # The roofline denominator follows what the clocks saw during the timed region: the sustained
+    # (power-capped) cuBLAS figure when sw_power_cap was active, the burst figure otherwise.
+    power_capped = "sw_power_cap" in sampler.reasons
+    peak = peaks["sustained"] if power_capped else peaks["burst"]
 
     e2e = None
     if not args.no_e2e:
@@ -593,8 +673,10 @@ def main():
                         if W.get("pipe") is not None else "pinned host -> device copies + C-ABI call + D -> pinned host")}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = oracle_baseline(W["oracle_case"])
+        if world > 1:
+            cpu["sample"] += f"; rank 0's inputs, timed after the GPU region while the other {world - 1} rank(s) wait"
 
     if rank == 0:
         kinfo = cy.last_kernel_info() if args.workload != "attention" else None
@@ -604,23 +686,28 @@ def main():
             "scaling": scaling_of(args.workload), "vs_baseline": None, "dtype": "f16",
             "data": "synthetic: seeded uniform[-1,1] rounded to fp16 (synth/), PCG64",
             "config": {"workload": W["desc"], **W["shape"],
-                       "parallelism": (f"batch shards x{world}, no collective" if args.workload in ("batched", "attention")
-                                       else f"M-row shards x{world}, B replicated, no collective" if args.workload != "allgather"
-                                       else f"M-row shards x{world} + NCCL all-gather"),
-                       "l2": "inputs rotate over 2 sets (> 126 MB L2 total)" if W["flops"] > 1e12 or args.workload == "batched" else "inputs rotate over 2 sets",
+                       "parallelism": (f"batch shards x{world}, no collective" if args.workload in ("batched", "batched-beta1", "attention")
+                                       else f"M-row shards x{world}, B replicated, D and y exchanged by chunked NCCL point-to-point overlapped with the compute"
+                                       if args.workload == "allgather"
+                                       else f"M-row shards x{world}, B replicated, fused replication (epilogue peer stores, device barriers)"
+                                       if args.workload == "allgather-fused"
+                                       else f"M-row shards x{world}, B replicated, no collective"),
+                       "l2": W["l2"],
                        "kernel_config": (kinfo if args.workload != "attention" else
                                          "attn_fwd_kernel: 2 x 128-row query tiles per CTA, 128-key blocks, TMEM S/P/O, 12 warps (setmaxnreg 208/72)")},
             "pct_of_dense_peak": round(100.0 * value / world / peak, 2),
             "pct_of_nominal_2250": round(100.0 * value / world / 2250.0, 2),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": load_traffic(args.workload),
-                         "peak_source": peaks["source"] + ("; sustained figure (timed region >= 0.5 s of back-to-back launches)"
-                                                           if long_region else "; burst figure (short timed region)"),
+                         "peak_source": peaks["source"] + ("; sustained figure (sw_power_cap active during the timed region)"
+                                                           if power_capped else "; burst figure (no power-cap reason during the timed region)"),
                          "frac_of_burst": round(achieved / peaks["burst"], 4),
                          "frac_of_sustained": round(achieved / peaks["sustained"], 4),
                          "kernel_ms": round(kern_ms, 5)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "exchange": ({**W["exchange"], "compute_ms_at_peak": round(W["kernel_flops"] / (peak * 1e12) * 1e3, 4),
+                          "measured_ms_per_step": round(ms_per_step, 4)} if "exchange" in W else None),
             "step_ms": step_stats(per),
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
@@ -636,7 +723,9 @@ def main():
 
 def reference_arm(args, rank, world):
     """--impl reference: the fp64 CPU oracle (the only reference this tier has), timed as it
-    stands on the host cores, on a bounded sample of the same workload per step."""
+    stands on the host cores, each step a bounded sample of the same workload: >= 512 output rows
+    (all columns, full K) or, batched, whole GEMMs of the batch -- the same sampling as the
+    cpu_baseline leg of the GPU arm, so the two agree."""
     if rank != 0:
         return
     import numpy as np
@@ -646,45 +735,25 @@ def reference_arm(args, rank, world):
 
     oracle.build()
     oracle.set_threads(len(os.sched_getaffinity(0)))  # torchrun sets OMP_NUM_THREADS=1
+    nth = oracle.num_threads()
     name = args.workload
     if name == "gemm" or name.startswith("sweep-"):
         n = 8192 if name == "gemm" else int(name.split("-")[1])
-        A = synth.uniform((n, n), synth.seed_for(1, 0))
-        B = synth.uniform((n, n), synth.seed_for(1, 1000))
-        per_row = 2.0 * n * n
-        fn = lambda rows: oracle.gemm("f16", A, B, rows=rows)  # noqa: E731
-        m = n
+        case = ("gemm", (synth.uniform((n, n), synth.seed_for(1, 0)), synth.uniform((n, n), synth.seed_for(1, 1000))))
         desc = f"fp16 GEMM {n}^3" + (f" x{world} M-shards" if world > 1 else "")
-    elif name in ("rowreduce", "allgather"):
-        m, n = 65536, 8192
-        A = synth.uniform((2048, n), synth.seed_for(4, 0))  # the sampled rows come from this block
-        B = synth.uniform((n, n), synth.seed_for(1, 1000))
-        per_row = 2.0 * n * n + n
-
-        def fn(rows):
-            oracle.gemm("f16", A, B, rows=rows % A.shape[0])
-            oracle.rowsum("f16", A, rows=rows % A.shape[0])
-        desc = "fp16 GEMM 65536 x 8192 x 8192 + row reduction"
-    elif name == "batched":
-        A = synth.uniform((64, 1024, 1024), synth.seed_for(2, 0))
-        B = synth.uniform((64, 1024, 1024), synth.seed_for(2, 1))
-        # sample unit = one whole 1024^3 GEMM of the batch (as the bench's cpu_baseline does)
-        per_row = 2.0 * 1024 ** 3
-        m = 64
-
-        def fn(rows):
-            for r in rows:
-                oracle.gemm("f16", A[r], B[r])
+    elif name in ("rowreduce", "allgather", "allgather-fused"):
+        # the sampled rows come from one 2048-row block of A (the oracle's cost per row is the same)
+        case = ("rowreduce" if name != "allgather-fused" else "gemm",
+                (synth.uniform((2048, 8192), synth.seed_for(4, 0)), synth.uniform((8192, 8192), synth.seed_for(1, 1000))))
+        desc = "fp16 GEMM 65536 x 8192 x 8192" + (" + row reduction" if name != "allgather-fused" else "")
+    elif name in ("batched", "batched-beta1"):
+        case = ("batched", (synth.uniform((64, 1024, 1024), synth.seed_for(2, 0)),
+                            synth.uniform((64, 1024, 1024), synth.seed_for(2, 1))))
         desc = "batched fp16 GEMM 64 x 1024^3"
-    elif name == "glu":
+    elif name in ("glu", "dual"):
         n = 8192
-        A = synth.uniform((n, n), synth.seed_for(3, 0))
-        B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
-        B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
-        per_row = 4.0 * n * n
-        m = n
-        fn = lambda rows: oracle.dual_glu("f16", "silu", A, B0, B1, rows=rows)  # noqa: E731
-        desc = "GLU dual-GEMM silu(A*B0)*(A*B1) 8192^3"
+        case = (name, tuple(synth.uniform((n, n), synth.seed_for(3, j)) for j in (0, 1001, 1002)))
+        desc = "GLU dual-GEMM silu(A*B0)*(A*B1) 8192^3" if name == "glu" else "dual-GEMM pair 8192^3"
     elif name == "attention":
         bsz, h, s_len, d = 2, 16, 8192, 128
         Q, K, V = (synth.uniform((bsz * h, s_len, d), synth.seed_for(6, t)) for t in range(3))
@@ -708,36 +777,28 @@ def reference_arm(args, rank, world):
                "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out), flush=True)
         return
-    elif name == "dual":
-        n = 8192
-        A = synth.uniform((n, n), synth.seed_for(3, 0))
-        B0 = synth.uniform((n, n), synth.seed_for(3, 1001))
-        B1 = synth.uniform((n, n), synth.seed_for(3, 1002))
-        per_row = 4.0 * n * n
-        m = n
-        fn = lambda rows: oracle.dual_gemm("f16", "pair", A, B0, B1, rows=rows)  # noqa: E731
-        desc = "dual-GEMM pair 8192^3"
     else:
         raise SystemExit(f"unknown workload {name}")
-    nth = oracle.num_threads()
-    # size each step to ~2 s of CPU work so K + W steps end within a few minutes
-    probe = np.arange(max(nth, 4))
-    t0 = time.perf_counter()
-    fn(probe)
-    dt0 = time.perf_counter() - t0
-    rows_per_step = int(max(len(probe), min(m, len(probe) * 2.0 / max(dt0, 1e-3))))
+    kind = case[0]
+    fn, per_unit, m, unit = oracle_unit_fn(*case)
+    fixed, per, p1 = oracle_calibrate(fn, m, nth)
+    # each step: >= 512 rows (batched: >= 1 GEMM), sized to ~4 s of CPU work so that the fixed
+    # per-call cost (operand decode) stays a small share, as in the cpu_baseline leg
+    floor = 1 if kind == "batched" else min(m, 512)
+    units_per_step = int(min(m, max(floor, (4.0 - fixed) / per)))
     steps = min(args.steps, 10)
     warm = min(args.warmup, 3)
     rng = np.random.default_rng(0)
+    warm_units = int(min(m, max(1, (1.0 - fixed) / per)))
     for _ in range(warm):
-        fn(np.sort(rng.choice(m, rows_per_step, replace=False)))
+        fn(np.sort(rng.choice(m, warm_units, replace=False)))
     t0 = time.perf_counter()
     for _ in range(steps):
-        fn(np.sort(rng.choice(m, rows_per_step, replace=False)))
+        fn(np.sort(rng.choice(m, units_per_step, replace=False)))
     dt = time.perf_counter() - t0
-    value = per_row * rows_per_step * steps / dt / 1e12
-    unit = "random batch GEMMs (1024^3 each)" if name == "batched" else "random rows (all columns, full K)"
-    sample = f"{rows_per_step} {unit} per step of {desc}; {steps} steps in {dt:.1f} s"
+    value = per_unit * units_per_step * steps / dt / 1e12
+    sample = (f"{units_per_step} random {unit} per step of {desc}; {steps} steps in {dt:.1f} s "
+              f"(calibrated fixed cost per call {fixed:.2f} s, {per * 1e3:.2f} ms per unit)")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
            "scaling": scaling_of(name), "vs_baseline": None, "dtype": "f64",

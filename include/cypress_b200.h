@@ -24,7 +24,8 @@
  *    and rounds ONCE to the output type with IEEE round-to-nearest-even
  *    (R3, R7).  Boundary tiles are handled in-kernel (zero-filled loads,
  *    clipped stores, R8): no element outside [0,m) x [0,n) is written.
- *  - m == 0 or n == 0 (or batch == 0): CY_OK, nothing launched.
+ *  - m == 0 or n == 0 (or batch == 0): CY_OK, nothing launched (except cy_gemm_rowreduce with
+ *    n == 0, which still computes y).
  *    k == 0: D = beta*C (y = 0), computed by the same kernel.
  *  - Hardware rules (TMA): every base pointer 16-byte aligned; every ld and
  *    stride a multiple of 8 elements (16 bytes), else CY_ERR_MISALIGNED.
@@ -100,6 +101,22 @@ cy_status_t cy_gemm_replicated(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, f
                                const void* C, int64_t ldc, void* const* D_dst, int ndst, int64_t ldd,
                                int64_t row_offset, int64_t rows_total, void* stream);
 
+/* Device-side barrier between the ranks of a job that share memory through peer mappings (CUDA IPC
+ * over NVLink / NVSwitch): the synchronisation step of the fused replicated GEMM (SURVEY NEXT-2 and
+ * 8(e); BASELINE configs[4] "+ all-gather").  dist.py runs, on every rank's stream,
+ *   cy_peer_barrier -> cy_gemm_replicated -> cy_peer_barrier
+ * (peers are done reading the previous result; then every peer's tile stores have landed).
+ * flags[j] (j < world): rank j's array of at least `world` uint32 flags, zero before first use,
+ * 4-byte aligned, mapped into this process (flags[rank] is this rank's own).  `epoch` is 1 on the
+ * first call and grows by one per call, identically on every rank.  One 32-thread kernel on
+ * `stream`: thread j fences system-wide, stores epoch into flags[j][rank] (release, system scope)
+ * and waits until flags[rank][j] >= epoch (acquire).  Launched without programmatic serialisation,
+ * so it starts only after the preceding work on `stream` has completed.  A peer that never
+ * arrives makes the kernel trap after ~60 s (the fault surfaces on the stream) instead of hanging.
+ * world in 1..8, 0 <= rank < world, epoch != 0, no NULL flag pointer, else CY_ERR_INVALID_VALUE;
+ * a flag pointer that is not 4-byte aligned: CY_ERR_MISALIGNED. */
+cy_status_t cy_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream);
+
 /* GLU activation for cy_dual_gemm_glu. */
 typedef enum { CY_ACT_SILU = 0, CY_ACT_GELU_TANH = 1 } cy_act_t;
 
@@ -115,7 +132,9 @@ cy_status_t cy_dual_gemm_glu(cy_dtype_t dt, cy_act_t act, int64_t m, int64_t n, 
 /* GEMM + row reduction: "C = A.B and y(i) = sum_k A(i,k)" in a single kernel,
  * the reduction done on SIMT warps from the shared-memory A tiles while the
  * tensor core computes A.B.  y: m floats (fp32, device),
- * unscaled and independent of B/alpha/beta/C (R2); must not overlap D. */
+ * unscaled and independent of B/alpha/beta/C (R2); must not overlap D.
+ * y(i) is summed in fp32 in k order.  n == 0 (no D): y alone is computed by a row-sum kernel with
+ * the same order (B, C, D are not touched and may be NULL); k == 0: y = 0. */
 cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha,
                               const void* A, int64_t lda, const void* B, int64_t ldb, float beta,
                               const void* C, int64_t ldc, void* D, int64_t ldd, float* y,

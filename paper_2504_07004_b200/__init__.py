@@ -76,8 +76,7 @@ def _stream(stream, dev):
 
 
 def _check_dev(*ts):
-    """All tensors must live on one CUDA device, which becomes the current device (the C ABI works
-    on the current device, torch semantics).  Returns the device index.  Uses get_device() (an int)
+    """All tensors must live on one CUDA device; returns its index.  Uses get_device() (an int)
     rather than .device objects: this runs on every call."""
     dev = -2
     for t in ts:
@@ -90,27 +89,70 @@ def _check_dev(*ts):
             dev = g
         elif g != dev:
             raise ValueError(f"cypress_b200: tensors on different devices (cuda:{dev} vs cuda:{g})")
-    if dev >= 0:
-        torch = _torch()
-        if torch.cuda.current_device() != dev:
-            torch.cuda.set_device(dev)
     return dev
+
+
+class _on_device:
+    """The C ABI works on the CURRENT device: make ``dev`` current for the call and restore the
+    caller's device afterwards (torch semantics; a no-op when it is already current)."""
+
+    __slots__ = ("dev", "prev")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.prev = -1
+
+    def __enter__(self):
+        if self.dev >= 0:
+            torch = _torch()
+            cur = torch.cuda.current_device()
+            if cur != self.dev:
+                self.prev = cur
+                torch.cuda.set_device(self.dev)
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev >= 0:
+            _torch().cuda.set_device(self.prev)
+        return False
+
+
+def _same_dtype(ref, *named):
+    for t, name in named:
+        if t is not None and t.dtype != ref.dtype:
+            raise ValueError(f"cypress_b200: {name} is {t.dtype}, A is {ref.dtype} (one 16-bit type for all operands)")
+
+
+def _shape(t, want, name):
+    if t is not None and tuple(t.shape) != tuple(want):
+        raise ValueError(f"cypress_b200: {name} has shape {tuple(t.shape)}, expected {tuple(want)}")
+
+
+def _mat2(A, B):
+    if A.dim() != 2 or B.dim() != 2:
+        raise ValueError("cypress_b200: A and B must be 2-D")
+    m, k = A.shape
+    if B.shape[0] != k:
+        raise ValueError(f"cypress_b200: inner dimensions differ (A is {tuple(A.shape)}, B is {tuple(B.shape)})")
+    return m, B.shape[1], k
 
 
 def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
     """D = alpha*A@B + beta*C  (A: m x k, B: k x n, row-major).  cy_gemm."""
-    torch = _torch()
     dev = _check_dev(A, B, C, out)
-    m, k = A.shape
-    n = B.shape[1]
-    if B.shape[0] != k:
-        raise ValueError("inner dimensions differ")
+    m, n, k = _mat2(A, B)
+    use_c = beta != 0
+    if use_c and C is None:
+        raise ValueError("cypress_b200: beta != 0 needs C")
+    _same_dtype(A, (B, "B"), (C if use_c else None, "C"), (out, "out"))
+    _shape(C if use_c else None, (m, n), "C")
+    _shape(out, (m, n), "out")
     if out is None:
         out = _empty2d(m, n, A)
-    lib = _lib.load()
-    st = lib.cy_gemm(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
-                     _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n,
-                     _ptr(out), _ld(out, "out"), _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_gemm(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"),
+                                 float(beta), _ptr(C) if use_c else None, _ld(C, "C") if use_c else n, _ptr(out),
+                                 _ld(out, "out"), _stream(stream, dev))
     check(st, "cy_gemm")
     return out
 
@@ -119,25 +161,36 @@ def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, 
     """D[b] = alpha*A[b]@B[b] + beta*C[b] for b < L (3-D tensors, rows contiguous)."""
     torch = _torch()
     dev = _check_dev(A, B, C, out)
+    if A.dim() != 3 or B.dim() != 3:
+        raise ValueError("cypress_b200: batched A and B must be 3-D (L, rows, cols)")
     L, m, k = A.shape
+    if B.shape[0] != L or B.shape[1] != k:
+        raise ValueError(f"cypress_b200: B has shape {tuple(B.shape)}, expected ({L}, {k}, n)")
     n = B.shape[2]
+    use_c = beta != 0
+    if use_c and C is None:
+        raise ValueError("cypress_b200: beta != 0 needs C")
+    _same_dtype(A, (B, "B"), (C if use_c else None, "C"), (out, "out"))
+    _shape(C if use_c else None, (L, m, n), "C")
+    _shape(out, (L, m, n), "out")
     if out is None:
         out = torch.empty((L, m, n), dtype=A.dtype, device=A.device)
 
     def lds(t):
         if t is None:
             return n, 0
-        if t.stride(2) != 1:
-            raise ValueError("rows must be contiguous")
+        if t.stride(2) != 1 and t.size(2) > 1:
+            raise ValueError("cypress_b200: rows must be contiguous")
         return t.stride(1), t.stride(0)
 
     lda, sa = lds(A)
     ldb, sb = lds(B)
-    ldc, sc = lds(C if beta != 0 else None)
+    ldc, sc = lds(C if use_c else None)
     ldd, sd = lds(out)
-    st = _lib.load().cy_gemm_batched(_dt(A), m, n, k, L, float(alpha), _ptr(A), lda, sa, _ptr(B), ldb, sb,
-                                     float(beta), _ptr(C) if beta != 0 else None, ldc, sc, _ptr(out), ldd, sd,
-                                     _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_gemm_batched(_dt(A), m, n, k, L, float(alpha), _ptr(A), lda, sa, _ptr(B), ldb, sb,
+                                         float(beta), _ptr(C) if use_c else None, ldc, sc, _ptr(out), ldd, sd,
+                                         _stream(stream, dev))
     check(st, "cy_gemm_batched")
     return out
 
@@ -146,24 +199,32 @@ def dual_gemm(A, B0, B1, C0=None, C1=None, alpha: float = 1.0, beta: float = 0.0
               out0=None, out1=None, stream=None):
     """mode "pair": (D0, D1) = (alpha*A@B0 + beta*C0, alpha*A@B1 + beta*C1);
     mode "sum": D = alpha*(A@B0 + A@B1) + beta*C0.  cy_dual_gemm."""
-    torch = _torch()
     dev = _check_dev(A, B0, B1, C0, C1, out0, out1)
-    m, k = A.shape
-    n = B0.shape[1]
-    pair = mode == "pair"
     if mode not in ("pair", "sum"):
         raise ValueError("mode must be 'pair' or 'sum'")
+    pair = mode == "pair"
+    m, n, k = _mat2(A, B0)
+    _shape(B1, (k, n), "B1")
+    use_c = beta != 0
+    if use_c and (C0 is None or (pair and C1 is None)):
+        raise ValueError("cypress_b200: beta != 0 needs C0 (and C1 in pair mode)")
+    if not pair and (C1 is not None or out1 is not None):
+        raise ValueError("cypress_b200: sum mode takes no C1 / out1")
+    _same_dtype(A, (B0, "B0"), (B1, "B1"), (C0 if use_c else None, "C0"), (C1 if use_c else None, "C1"),
+                (out0, "out0"), (out1, "out1"))
+    for t, name in ((C0 if use_c else None, "C0"), (C1 if use_c else None, "C1"), (out0, "out0"), (out1, "out1")):
+        _shape(t, (m, n), name)
     if out0 is None:
         out0 = _empty2d(m, n, A)
     if pair and out1 is None:
         out1 = _empty2d(m, n, A)
-    use_c = beta != 0
-    st = _lib.load().cy_dual_gemm(
-        _dt(A), CY_DUAL_PAIR if pair else CY_DUAL_SUM, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
-        _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), float(beta), _ptr(C0) if use_c else None,
-        _ld(C0, "C0") if (use_c and C0 is not None) else n, _ptr(C1) if (use_c and pair) else None,
-        _ld(C1, "C1") if (use_c and pair and C1 is not None) else n, _ptr(out0), _ld(out0, "out0"),
-        _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_dual_gemm(
+            _dt(A), CY_DUAL_PAIR if pair else CY_DUAL_SUM, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
+            _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), float(beta), _ptr(C0) if use_c else None,
+            _ld(C0, "C0") if use_c else n, _ptr(C1) if (use_c and pair) else None,
+            _ld(C1, "C1") if (use_c and pair) else n, _ptr(out0), _ld(out0, "out0"),
+            _ptr(out1) if pair else None, _ld(out1, "out1") if pair else n, _stream(stream, dev))
     check(st, "cy_dual_gemm")
     return (out0, out1) if pair else out0
 
@@ -174,54 +235,90 @@ def attention(Q, K, V, scale=None, causal: bool = False, out=None, lse=None, str
     Returns (O, lse) with lse (batch, heads, seq_q) fp32 natural log-sum-exp.  cy_attention_fwd."""
     torch = _torch()
     dev = _check_dev(Q, K, V, out, lse)
+    if Q.dim() != 4 or K.dim() != 4 or V.dim() != 4:
+        raise ValueError("cypress_b200: Q, K, V must be 4-D (batch, heads, seq, head_dim)")
     b, h, sq, d = Q.shape
     sk = K.shape[2]
-    for t, name in ((Q, "Q"), (K, "K"), (V, "V")):
-        if not t.is_contiguous():
-            raise ValueError(f"{name} must be contiguous (batch, heads, seq, head_dim)")
+    if tuple(K.shape) != (b, h, sk, d):
+        raise ValueError(f"cypress_b200: K has shape {tuple(K.shape)}, expected ({b}, {h}, seq_k, {d}) "
+                         "(same batch, heads and head_dim as Q; no GQA/MQA broadcast)")
+    if tuple(V.shape) != tuple(K.shape):
+        raise ValueError(f"cypress_b200: V has shape {tuple(V.shape)}, expected K's {tuple(K.shape)}")
+    _same_dtype(Q, (K, "K"), (V, "V"), (out, "out"))
+    for t, name in ((Q, "Q"), (K, "K"), (V, "V"), (out, "out"), (lse, "lse")):
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"cypress_b200: {name} must be contiguous")
+    _shape(out, (b, h, sq, d), "out")
+    _shape(lse, (b, h, sq), "lse")
+    if lse is not None and lse.dtype != torch.float32:
+        raise ValueError("cypress_b200: lse must be float32")
     if scale is None:
         scale = d ** -0.5
     if out is None:
         out = torch.empty_like(Q)
     if lse is None:
         lse = torch.empty((b, h, sq), dtype=torch.float32, device=Q.device)
-    st = _lib.load().cy_attention_fwd(_dt(Q), b, h, sq, sk, d, float(scale), int(bool(causal)), _ptr(Q), _ptr(K),
-                                      _ptr(V), _ptr(out), _ptr(lse), _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_attention_fwd(_dt(Q), b, h, sq, sk, d, float(scale), int(bool(causal)), _ptr(Q),
+                                          _ptr(K), _ptr(V), _ptr(out), _ptr(lse), _stream(stream, dev))
     check(st, "cy_attention_fwd")
     return out, lse
 
 
 def gemm_replicated(A, B, dsts, row_offset: int, rows_total: int, C=None, alpha: float = 1.0, beta: float = 0.0,
-                    stream=None):
+                    ldd=None, stream=None):
     """Compute D_shard = alpha*A@B + beta*C and store it at rows [row_offset, row_offset + m) of every
-    destination in ``dsts`` (2-D tensors or raw device addresses of rows_total x n matrices, same ld).
+    destination in ``dsts`` (2-D tensors or raw device addresses of rows_total x n matrices with
+    leading dimension ``ldd``; taken from the first tensor if not given, required for raw addresses).
     cy_gemm_replicated (fused replication; the destinations are usually peers' buffers)."""
     import ctypes
 
     dev = _check_dev(A, B, C)
-    m, k = A.shape
-    n = B.shape[1]
-    ptrs = [d if isinstance(d, int) else d.data_ptr() for d in dsts]
-    ldd = next((_ld(d, "dst") for d in dsts if not isinstance(d, int)), (n + 7) // 8 * 8)
+    m, n, k = _mat2(A, B)
+    use_c = beta != 0
+    if use_c and C is None:
+        raise ValueError("cypress_b200: beta != 0 needs C")
+    _same_dtype(A, (B, "B"), (C if use_c else None, "C"))
+    _shape(C if use_c else None, (m, n), "C")
+    ptrs = []
+    for d in dsts:
+        if isinstance(d, int):
+            ptrs.append(d)
+            continue
+        _same_dtype(A, (d, "dst"))
+        _shape(d, (rows_total, n), "dst")
+        if ldd is None:
+            ldd = _ld(d, "dst")
+        elif _ld(d, "dst") != ldd:
+            raise ValueError("cypress_b200: every destination must have leading dimension ldd")
+        ptrs.append(d.data_ptr())
+    if ldd is None:
+        raise ValueError("cypress_b200: raw destination addresses need ldd")
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
-    st = _lib.load().cy_gemm_replicated(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"),
-                                        float(beta), _ptr(C) if beta != 0 else None,
-                                        _ld(C, "C") if (C is not None and beta != 0) else n, arr, len(ptrs), ldd,
-                                        int(row_offset), int(rows_total), _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_gemm_replicated(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B),
+                                            _ld(B, "B"), float(beta), _ptr(C) if use_c else None,
+                                            _ld(C, "C") if use_c else n, arr, len(ptrs), int(ldd), int(row_offset),
+                                            int(rows_total), _stream(stream, dev))
     check(st, "cy_gemm_replicated")
 
 
 def dual_gemm_glu(A, B0, B1, act: str = "silu", alpha: float = 1.0, out=None, stream=None):
     """D = act(alpha*A@B0) * (alpha*A@B1), act in {"silu", "gelu_tanh"} (GLU).  cy_dual_gemm_glu."""
     dev = _check_dev(A, B0, B1, out)
-    m, k = A.shape
-    n = B0.shape[1]
+    m, n, k = _mat2(A, B0)
+    _shape(B1, (k, n), "B1")
+    _same_dtype(A, (B0, "B0"), (B1, "B1"), (out, "out"))
+    _shape(out, (m, n), "out")
+    if act not in ("silu", "gelu_tanh"):
+        raise ValueError("act must be 'silu' or 'gelu_tanh'")
     a = {"silu": _lib.CY_ACT_SILU, "gelu_tanh": _lib.CY_ACT_GELU_TANH}[act]
     if out is None:
         out = _empty2d(m, n, A)
-    st = _lib.load().cy_dual_gemm_glu(_dt(A), a, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
-                                      _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), _ptr(out), _ld(out, "out"),
-                                      _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_dual_gemm_glu(_dt(A), a, m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B0),
+                                          _ld(B0, "B0"), _ptr(B1), _ld(B1, "B1"), _ptr(out), _ld(out, "out"),
+                                          _stream(stream, dev))
     check(st, "cy_dual_gemm_glu")
     return out
 
@@ -230,16 +327,25 @@ def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None
     """D = alpha*A@B + beta*C and y[i] = sum_k A[i,k] (fp32), one kernel.  cy_gemm_rowreduce."""
     torch = _torch()
     dev = _check_dev(A, B, C, out, y)
-    m, k = A.shape
-    n = B.shape[1]
+    m, n, k = _mat2(A, B)
+    use_c = beta != 0
+    if use_c and C is None:
+        raise ValueError("cypress_b200: beta != 0 needs C")
+    _same_dtype(A, (B, "B"), (C if use_c else None, "C"), (out, "out"))
+    _shape(C if use_c else None, (m, n), "C")
+    _shape(out, (m, n), "out")
+    _shape(y, (m,), "y")
+    if y is not None and (y.dtype != torch.float32 or (m > 1 and y.stride(0) != 1)):
+        raise ValueError("cypress_b200: y must be a contiguous float32 vector")
     if out is None:
         out = _empty2d(m, n, A)
     if y is None:
         y = torch.empty((m,), dtype=torch.float32, device=A.device)
-    st = _lib.load().cy_gemm_rowreduce(
-        _dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
-        _ptr(C) if beta != 0 else None, _ld(C, "C") if (C is not None and beta != 0) else n, _ptr(out),
-        _ld(out, "out"), _ptr(y), _stream(stream, dev))
+    with _on_device(dev):
+        st = _lib.load().cy_gemm_rowreduce(
+            _dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"), float(beta),
+            _ptr(C) if use_c else None, _ld(C, "C") if use_c else n, _ptr(out),
+            _ld(out, "out") if n > 0 else max(8, out.stride(0)), _ptr(y), _stream(stream, dev))
     check(st, "cy_gemm_rowreduce")
     return out, y
 

@@ -11,12 +11,13 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcypress_b200.so")
+_PRODUCT_PATH = LIB_PATH
 
 # Every symbol include/cypress_b200.h declares (checked by tests/test_abi_cpu.py).
 EXPORTS = (
     "cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce", "cy_status_string",
     "cy_num_configs", "cy_config_info", "cy_force_config", "cy_last_config", "cy_launch_count",
-    "cy_last_kernel_info", "cy_gemm_replicated", "cy_attention_fwd",
+    "cy_last_kernel_info", "cy_gemm_replicated", "cy_attention_fwd", "cy_peer_barrier",
 )
 
 CY_OK = 0
@@ -35,6 +36,15 @@ class CyError(RuntimeError):
 
 
 _lib = None
+
+
+def use_library(path: str) -> None:
+    """Timing experiments only (scripts/): load an experiment build instead of the product library.
+    Must run before the first call; tests, smoke() and bench.py never use it."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("library already loaded")
+    LIB_PATH = path
 
 
 def load():
@@ -57,6 +67,11 @@ def load():
                                        ctypes.POINTER(ctypes.c_void_p), ci, i64, i64, i64, vp]
     lib.cy_attention_fwd.argtypes = [ci, i64, i64, i64, i64, i64, f32, ci, vp, vp, vp, vp, vp, vp]
     lib.cy_attention_fwd.restype = ci
+    if LIB_PATH != _PRODUCT_PATH and not hasattr(lib, "cy_peer_barrier"):
+        pass  # an older experiment build (scripts/): no peer barrier
+    else:
+        lib.cy_peer_barrier.argtypes = [ctypes.POINTER(ctypes.c_void_p), ci, ci, ctypes.c_uint32, vp]
+        lib.cy_peer_barrier.restype = ci
     lib.cy_gemm_rowreduce.argtypes = [ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, i64,
                                       vp, vp]
     for f in ("cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce",

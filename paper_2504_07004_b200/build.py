@@ -22,16 +22,22 @@ def sources():
                   [os.path.join(ROOT, "include", "cypress_b200.h")])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(OUT) or any(os.path.getmtime(s) > os.path.getmtime(OUT) for s in sources())
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT) -> str:
+    """Compile the product library (no ``defines``) or, for timing experiments only, a separate
+    library at ``out`` with extra ``-D`` switches (scripts/build_experiment.py).  The product
+    library never carries experiment switches."""
+    if defines and out == OUT:
+        raise ValueError("experiment switches must go to a separate library, not the product .so")
+    stale = force or not os.path.exists(out) or any(os.path.getmtime(s) > os.path.getmtime(out) for s in sources())
     if stale:
-        tmp = OUT + f".tmp{os.getpid()}"
-        cmd = [NVCC, *FLAGS, os.path.join(CSRC, "cy_gemm.cu"), os.path.join(CSRC, "cy_attention.cu"), "-o", tmp]
+        tmp = out + f".tmp{os.getpid()}"
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], os.path.join(CSRC, "cy_gemm.cu"),
+               os.path.join(CSRC, "cy_attention.cu"), os.path.join(CSRC, "cy_comm.cu"), "-o", tmp]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
-        os.replace(tmp, OUT)
-    return OUT
+        os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

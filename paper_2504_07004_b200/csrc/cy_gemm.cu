@@ -88,11 +88,6 @@ const int g_l2_policy = [] {
   const char* e = std::getenv("CY_L2_POLICY");
   return e ? std::atoi(e) : 5;
 }();
-// CY_DEBUG_MODE: timing experiments only (invalid results); never set in production
-const int g_debug = [] {
-  const char* e = std::getenv("CY_DEBUG_MODE");
-  return e ? std::atoi(e) : 0;
-}();
 // CY_SCHED: 0 = dynamic (cluster launch control) when there is more than one wave, 1 = static
 const int g_sched = [] {
   const char* e = std::getenv("CY_SCHED");
@@ -337,7 +332,6 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.tiles = (int)(L * p.m_blocks * p.n_blocks);
   p.group_m = g_group_m > 0 ? g_group_m : 8;
   p.l2_policy = g_l2_policy;
-  p.debug = g_debug;
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
   p.act = act;
@@ -414,6 +408,46 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
 }
 
 bool ld_ok(int64_t ld) { return ld > 0 && (ld % 8) == 0; }
+
+// y(i) = sum_k A(i,k) alone, for cy_gemm_rowreduce with n == 0 (no output tiles, so no reducer
+// warps run; P:1579 still defines y).  One thread per row adds in k order in fp32 -- the order and
+// precision of the fused reducer warps (cy_kernel.cuh), so y is bit-identical to the n > 0 path.
+template <int DT>
+__global__ void __launch_bounds__(128) rowsum_kernel(const uint16_t* __restrict__ A, int64_t lda, int m, int k,
+                                                     float* __restrict__ y) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= m) return;
+  const uint16_t* a = A + static_cast<int64_t>(row) * lda;
+  float acc = 0.f;
+  int kk = 0;
+  for (; kk + 8 <= k; kk += 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(a + kk);  // 16-B aligned: A and lda*2 are
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = cy::unpack2<DT>(w[e]);
+      acc += f.x;
+      acc += f.y;
+    }
+  }
+  for (; kk < k; ++kk) acc += cy::unpack2<DT>(static_cast<uint32_t>(a[kk])).x;
+  y[row] = acc;
+}
+
+cy_status_t launch_rowsum(int dt, const void* A, int64_t lda, int64_t m, int64_t k, float* y, void* stream) {
+  int dev;
+  DevState* st;
+  cy_status_t s = device_state(dev, st);
+  if (s != CY_OK) return s;
+  if (m > INT32_MAX || k > INT32_MAX) return CY_ERR_INVALID_VALUE;
+  const dim3 grid(static_cast<unsigned>((m + 127) / 128));
+  auto* a = static_cast<const uint16_t*>(A);
+  if (dt == 0) rowsum_kernel<0><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a, lda, (int)m, (int)k, y);
+  else rowsum_kernel<1><<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a, lda, (int)m, (int)k, y);
+  if (cudaGetLastError() != cudaSuccess) return CY_ERR_LAUNCH;
+  g_launches.fetch_add(1);
+  return CY_OK;
+}
 
 }  // namespace
 
@@ -626,7 +660,13 @@ cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, fl
   if (s != CY_OK) return s;
   if (m == 0) return CY_OK;
   if (!y) return CY_ERR_INVALID_VALUE;
-  if (n == 0) return CY_ERR_INVALID_VALUE;  // y is produced by the n-tile-0 CTAs; n == 0 has no tiles
+  if (n == 0) {  // no D tiles; y is still defined: the stand-alone row-sum kernel
+    if (k > 0 && !A) return CY_ERR_INVALID_VALUE;
+    if (k > 0 && lda < k) return CY_ERR_INVALID_VALUE;
+    if ((reinterpret_cast<uintptr_t>(y) & 3u) || (k > 0 && (!aligned16(A) || !ld_ok(lda)))) return CY_ERR_MISALIGNED;
+    if (k > 0 && overlap(span(y, 1, m, m, 1, 0, 4), span(A, m, k, lda, 1, 0, 2))) return CY_ERR_INVALID_VALUE;
+    return launch_rowsum(dt, A, lda, m, k, y, stream);
+  }
   const bool has_c = beta != 0.0f;
   if (!D || (k > 0 && (!A || !B)) || (has_c && !C)) return CY_ERR_INVALID_VALUE;
   if (ldd < n || (k > 0 && (lda < k || ldb < n)) || (has_c && ldc < n)) return CY_ERR_INVALID_VALUE;

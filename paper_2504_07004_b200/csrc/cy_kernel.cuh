@@ -31,7 +31,17 @@
 
 #include "cy_ptx.cuh"
 
+// CY_DEBUG_MODE: timing experiments only (results INVALID): 1 = no TMA refill, 2 = no epilogue,
+// 4 = no D stores, 8 = TMEM loads only.  Compile-time only: the product library is always built
+// with 0 (nothing at run time can switch it on); scripts/build_experiment.py builds a separate
+// library with it set.
+#ifndef CY_DEBUG_MODE
+#define CY_DEBUG_MODE 0
+#endif
+
 namespace cy {
+
+constexpr int kDebug = CY_DEBUG_MODE;
 
 enum Variant : int { V_GEMM = 0, V_DUAL_PAIR = 1, V_DUAL_SUM = 2, V_ROWREDUCE = 3, V_DUAL_GLU = 4 };
 
@@ -44,7 +54,6 @@ struct Params {
   int group_m;           // grouped rasterisation width (in m-blocks)
   int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
-  int debug;             // timing experiments only (results invalid): 1 = no TMA refill, 2 = no epilogue
   int act;               // V_DUAL_GLU: 0 = SiLU, 1 = GELU (tanh form)
   int n_extra;           // number of extra D destinations in DstMaps (0 = D only)
   int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           mbar_wait(bEmpty + 8 * stage, phase ^ 1);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
-          if ((p.debug & 1) && (phase || i != 0)) {  // timing experiment: reuse stale stages
+          if ((kDebug & 1) && (phase || i != 0)) {  // timing experiment: reuse stale stages
             if (PAIR_TMA ? rank == 0 : true) mbar_arrive(fb);  // (MC == 1 only)
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             continue;
@@ -473,24 +482,49 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
   } else if (warp < 2 + C::EPI_WARPS) {
     // ------------------------------------------------------------------ epilogue
+    // Per warp and tile, a fixed list of 32-row x 64-column chunks: q -> (accumulator a, chunk c).
+    // The warp's chunks of one accumulator are loaded from TMEM in groups of G before the
+    // accumulator is handed back (G = 2 when TMEM is single-buffered, so the MMA issuer waits only
+    // for the loads, not for the conversions and stores); with two staging slots the C tile of the
+    // next chunk is fetched while the current one is converted and stored.
+    constexpr int NCH = C::BN / 64;                 // 64-column chunks per accumulator
+    constexpr int CPW = NCH / C::EPI_SPLIT;         // chunks per warp per accumulator
+    constexpr int G = (C::EPI_SPLIT == 2 && !C::GLU && !C::REDUCE && CPW == 2) ? 2 : 1;
+    constexpr int NQ = C::NUM_OUT * CPW;            // chunks per warp per tile
+    constexpr bool CPF = (C::EPI_BUFS == 2);        // C prefetch one chunk ahead
     const int ew = warp - 2;
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q4 = warp & 3;  // TMEM lane quarter this warp may access
     const int half = ew / 4;  // EPI_SPLIT == 2: this warp takes chunks c with c % 2 == half
     const uint32_t sE = sEpi + ew * C::EPI_BUFS * C::EPI_BUF_BYTES;
     const uint32_t cbar = bCBar + 8 * ew;
     const uint64_t pol = policy_evict_normal();
     uint32_t slot = 0, cphase = 0;
+    auto chunk_col = [&](int q) { return (C::EPI_SPLIT == 2 ? half : 0) + (q % CPW) * C::EPI_SPLIT; };
+    // column of chunk q in the output; C/D maps of chunk q
+    auto chunk_n0 = [&](int nb, int q) { return nb * C::TILE_N + (C::DUAL ? 0 : (q / CPW) * C::BN) + 64 * chunk_col(q); };
+    auto chunk_c = [&](int q) { return (C::VAR == V_DUAL_PAIR && q / CPW == 1) ? &tmC1 : &tmC0; };
+    auto chunk_d = [&](int q) { return (C::VAR == V_DUAL_PAIR && q / CPW == 1) ? &tmD1 : &tmD0; };
+    // lane 0: wait until slot `s` may be overwritten (the store that last used it has read it) and
+    // fetch chunk q's C tile into it
+    auto fetch_c = [&](int nb, int row0, int b, int q, uint32_t s) {
+      if (lane == 0) {
+        bulk_wait_read<C::EPI_BUFS - 1>();
+        mbar_arrive_expect_tx(cbar, C::EPI_BUF_BYTES);
+        tma_load_3d(sE + s * C::EPI_BUF_BYTES, chunk_c(q), cbar, chunk_n0(nb, q), row0, b, pol);
+      }
+    };
     int t;
     for (int it = 0; sched_next(it, t, true); ++it) {
       int b, mb, nb;
       tile_coords(p, t, b, mb, nb);
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
+      const int row0 = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA + 32 * q4;
+      if (CPF && p.has_c) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
       if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
       else mbar_wait(bTFull + 8 * buf, bph);
       tc_fence_after();
-      const int row0 = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA + 32 * q;
-      if (p.debug & 2) {  // timing experiment: drop the epilogue
+      if constexpr ((kDebug & 2) != 0) {  // timing experiment: drop the epilogue
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -502,95 +536,143 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
         continue;
       }
-#pragma unroll 1
-      for (int a = 0; a < C::NUM_OUT; ++a) {
-        const bool second = (C::VAR == V_DUAL_PAIR && a == 1);
-        const CUtensorMap* tmD = second ? &tmD1 : &tmD0;
-        const CUtensorMap* tmC = second ? &tmC1 : &tmC0;
-#pragma unroll 1
-        for (int c = (C::EPI_SPLIT == 2 ? half : 0); c < C::BN / 64; c += C::EPI_SPLIT) {
-          const int n0 = nb * C::TILE_N + (C::DUAL ? 0 : a * C::BN) + 64 * c;
-          const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
+      // TMEM lane quarter q4, accumulator a, 64 columns of chunk q (two x32 loads)
+      auto tmem_chunk = [&](int a, int q) {
+        return tmem_base + (uint32_t(32 * q4) << 16) + buf * C::ACC_COLS + a * C::BN + 64 * chunk_col(q);
+      };
+      auto release = [&](int a) {  // accumulator a (buffer `buf`) is in registers: hand TMEM back
+        if (C::SPLIT || a == C::NUM_OUT - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
+            if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, leader));
+            else mbar_arrive(bar);
+          }
+        }
+      };
+      // wait until the current slot may be written (no C) / holds chunk q's C tile
+      auto slot_ready = [&](int q) {
+        if (p.has_c) {
+          if (!CPF) fetch_c(nb, row0, b, q, slot);
+          mbar_wait(cbar, cphase);
+          cphase ^= 1;
+        } else {
           if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // the store that last used this slot has read it
           __syncwarp();
-          if (p.has_c) {
-            if (lane == 0) {
-              mbar_arrive_expect_tx(cbar, C::EPI_BUF_BYTES);
-              tma_load_3d(sb, tmC, cbar, n0, row0, b, pol);
-            }
-            mbar_wait(cbar, cphase);
-            cphase ^= 1;
-          }
-          uint32_t r0[32], r1[32];
-          uint32_t g0[C::GLU ? 32 : 1], g1[C::GLU ? 32 : 1];  // GLU: the gate operand (accumulator 1)
-          if (p.k_blocks > 0) {
-            const uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + buf * C::ACC_COLS + a * C::BN + 64 * c;
-            tmem_ld_32x32b_x32(ta, r0);
-            tmem_ld_32x32b_x32(ta + 32, r1);
-            if constexpr (C::GLU) {
-              tmem_ld_32x32b_x32(ta + C::BN, g0);
-              tmem_ld_32x32b_x32(ta + C::BN + 32, g1);
-            }
-            tmem_ld_wait();
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r0[i] = r1[i] = 0u;
-            if constexpr (C::GLU) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) g0[i] = g1[i] = 0u;
-            }
-          }
-          // The last chunk of this accumulator (buffer) is in registers: hand the TMEM columns back
-          // to the MMA issuer before converting and storing it.
-          if (c + C::EPI_SPLIT >= C::BN / 64 && (C::SPLIT || a == C::NUM_OUT - 1)) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
-              if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, leader));
-              else mbar_arrive(bar);
-            }
-          }
-          if (p.debug & 8) continue;  // timing experiment: TMEM loads only
-          const uint32_t row_addr = sb + lane * 128;
-          const bool unit_alpha = (p.alpha == 1.0f);
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const uint32_t addr = row_addr + ((v ^ (lane & 7)) << 4);  // SWIZZLE_128B chunk
-            float f[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int col = 8 * v + e;
-              const float x = __uint_as_float(col < 32 ? r0[col] : r1[col - 32]);
-              f[e] = unit_alpha ? x : x * p.alpha;
-              if constexpr (C::GLU) {
-                const float gx = __uint_as_float(col < 32 ? g0[col] : g1[col - 32]);
-                const float u = unit_alpha ? gx : gx * p.alpha;
-                f[e] = act_f32(p.act, f[e]) * u;
-              }
-            }
-            if (p.has_c) {
-              uint32_t cv[4];
-              ld_shared_v4(addr, cv[0], cv[1], cv[2], cv[3]);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 cf = unpack2<C::DT>(cv[e]);
-                f[2 * e] = fmaf(p.beta, cf.x, f[2 * e]);
-                f[2 * e + 1] = fmaf(p.beta, cf.y, f[2 * e + 1]);
-              }
-            }
-            st_shared_v4(addr, pack2<C::DT>(f[0], f[1]), pack2<C::DT>(f[2], f[3]), pack2<C::DT>(f[4], f[5]),
-                         pack2<C::DT>(f[6], f[7]));
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && !(p.debug & 4)) {  // (debug 4: timing experiment without the D stores)
-            tma_store_3d(tmD, sb, n0, row0, b);
-            for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
-            bulk_commit();
-          }
-          if constexpr (C::EPI_BUFS == 2) slot ^= 1;
         }
+      };
+      auto store_chunk = [&](int q) {  // staging slot -> D (and the replicas), next slot, next C
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !(kDebug & 4)) {  // (debug 4: timing experiment without the D stores)
+          const int n0 = chunk_n0(nb, q);
+          const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
+          tma_store_3d(chunk_d(q), sb, n0, row0, b);
+          for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
+          bulk_commit();
+        }
+        if constexpr (C::EPI_BUFS == 2) slot ^= 1;
+        if (CPF && p.has_c && q + 1 < NQ) fetch_c(nb, row0, b, q + 1, slot);  // next chunk's C
+      };
+      const bool unit_alpha = (p.alpha == 1.0f);
+      if (G == 2 && !p.has_c) {
+        // beta == 0, single-buffered TMEM: both of this warp's chunks of an accumulator are loaded
+        // and rounded (alpha*acc, one RN cast) into 16-bit pairs before the accumulator is handed
+        // back, so the MMA issuer waits only for the TMEM loads.
+#pragma unroll 1
+        for (int a = 0; a < C::NUM_OUT; ++a) {
+          uint32_t pk[2][32];
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            uint32_t r[64];
+            if (p.k_blocks > 0) {
+              const uint32_t ta = tmem_chunk(a, a * CPW + g);
+              tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) r[i] = 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+              pk[g][i] = unit_alpha ? pack2<C::DT>(x0, x1) : pack2<C::DT>(x0 * p.alpha, x1 * p.alpha);
+            }
+          }
+          release(a);
+          if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            slot_ready(a * CPW + g);
+            const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              st_shared_v4(row_addr + ((v ^ (lane & 7)) << 4), pk[g][4 * v], pk[g][4 * v + 1], pk[g][4 * v + 2],
+                           pk[g][4 * v + 3]);
+            store_chunk(a * CPW + g);
+          }
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int q = 0; q < NQ; ++q) {
+        const int a = q / CPW;
+        uint32_t r[64];
+        uint32_t gt[C::GLU ? 64 : 1];  // GLU: the gate operand (accumulator 1)
+        if (p.k_blocks > 0) {
+          const uint32_t ta = tmem_chunk(a, q);
+          tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          if constexpr (C::GLU) {
+            tmem_ld_32x32b_x32(ta + C::BN, *reinterpret_cast<uint32_t(*)[32]>(&gt[0]));
+            tmem_ld_32x32b_x32(ta + C::BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&gt[32]));
+          }
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) r[i] = 0u;
+          if constexpr (C::GLU) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) gt[i] = 0u;
+          }
+        }
+        // The accumulator's last chunk is in registers: hand its TMEM columns back to the MMA
+        // issuer before converting and storing it.
+        if ((q + 1) % CPW == 0) release(a);
+        if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
+        slot_ready(q);
+        const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint32_t addr = row_addr + ((v ^ (lane & 7)) << 4);  // SWIZZLE_128B chunk
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = 8 * v + e;
+            const float x = __uint_as_float(r[col]);
+            f[e] = unit_alpha ? x : x * p.alpha;
+            if constexpr (C::GLU) {
+              const float gx = __uint_as_float(gt[col]);
+              const float u = unit_alpha ? gx : gx * p.alpha;
+              f[e] = act_f32(p.act, f[e]) * u;
+            }
+          }
+          if (p.has_c) {
+            uint32_t cv[4];
+            ld_shared_v4(addr, cv[0], cv[1], cv[2], cv[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 cf = unpack2<C::DT>(cv[e]);
+              f[2 * e] = fmaf(p.beta, cf.x, f[2 * e]);
+              f[2 * e + 1] = fmaf(p.beta, cf.y, f[2 * e + 1]);
+            }
+          }
+          st_shared_v4(addr, pack2<C::DT>(f[0], f[1]), pack2<C::DT>(f[2], f[3]), pack2<C::DT>(f[4], f[5]),
+                       pack2<C::DT>(f[6], f[7]));
+        }
+        store_chunk(q);
       }
     }
     if (lane == 0) bulk_wait_read<0>();  // shared staging must outlive the stores' reads

@@ -1,7 +1,7 @@
 """A/B attention throughput of library builds: python scripts/attn_ab.py LIB.so [LIB2.so ...]
 (each build is run in its own process by the caller; env knobs such as CY_ATTN_EMU are read per call)."""
 import sys, os
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 from paper_2504_07004_b200 import _lib
 _lib.LIB_PATH = os.path.abspath(sys.argv[1])

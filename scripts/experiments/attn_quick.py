@@ -1,6 +1,6 @@
 """Attention throughput at two shapes (env knobs such as CY_ATTN_EMU are read by the library)."""
 import sys, os
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 

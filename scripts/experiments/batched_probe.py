@@ -1,6 +1,6 @@
 """Batched L x 1024^3 probe (for ncu and timing)."""
 import sys, os
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8

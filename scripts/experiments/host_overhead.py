@@ -1,7 +1,7 @@
 """Host cost per call (no synchronisation inside the loop): the Python binding, the raw C-ABI call
 with pre-marshalled arguments, and torch.matmul (informational), at a tiny shape."""
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 from paper_2504_07004_b200 import _lib

@@ -1,6 +1,6 @@
 """Small-shape latency: host time per call (wall) and device time per launch (events), ours vs torch.matmul."""
 import sys, os, time
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 

@@ -1,7 +1,7 @@
 """M-shard probe: an m x 8192 x 8192 GEMM (the 8192^3 problem strong-scaled over 8192/m GPUs), every config
 forced vs the heuristic vs torch.matmul, device time per launch with the launches queued behind a long kernel."""
 import sys, os
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 from small_probe_util import dev_time

@@ -1,6 +1,6 @@
 """Small-shape device time per launch for every GEMM config (forced) vs the host heuristic and torch."""
 import sys, os
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 

@@ -1,7 +1,7 @@
 """What split-K would buy at small sizes, without building it: device time (CUDA-graph replay) of
 the per-split work alone (2 or 4 x the tiles at K/2 or K/4) vs the unsplit GEMM."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import torch
 import paper_2504_07004_b200 as cy
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))

@@ -42,6 +42,37 @@ def test_library_exports_every_declared_symbol(lib):
         assert hasattr(lib, s), s
 
 
+def test_library_exports_exactly_the_declared_symbols(lib):
+    """Every exported C symbol of the product library (nm -D, the cy_ prefix) is declared in
+    include/*.h and vice versa: no undeclared entry point (e.g. a trace hook) ships."""
+    import shutil
+    import subprocess
+
+    from paper_2504_07004_b200 import build
+
+    nm = shutil.which("nm")
+    if not nm:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "--defined-only", build.OUT], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if ln.split() and ln.split()[-1].startswith("cy_")
+                and " T " in ln}
+    assert exported == declared_symbols()
+
+
+def test_product_build_has_no_experiment_switches():
+    """Timing-experiment switches (CY_DEBUG_MODE: invalid results) are compile-time only and the
+    product build never sets them; the kernel reads no such run-time parameter."""
+    from paper_2504_07004_b200 import build
+
+    assert not any(f.startswith("-DCY_DEBUG") for f in build.FLAGS)
+    with pytest.raises(ValueError):
+        build.build(defines=("CY_DEBUG_MODE=1",))
+    src = open(os.path.join(ROOT, "paper_2504_07004_b200", "csrc", "cy_gemm.cu")).read()
+    assert "CY_DEBUG_MODE" not in src  # no getenv of it on the host side
+    kern = open(os.path.join(ROOT, "paper_2504_07004_b200", "csrc", "cy_kernel.cuh")).read()
+    assert "p.debug" not in kern
+
+
 def test_library_is_sm100a_and_uses_tcgen05():
     """The cubin inside the .so is sm_100a and contains tcgen05 MMA / TMA / TMEM loads."""
     import shutil

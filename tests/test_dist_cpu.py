@@ -94,8 +94,12 @@ def _worker(rank, world, port, q):
         A, B, _ = synth.gemm_inputs(m, n, k, seed=77, batch=L, kind="int")
         s, e, _ = shard_batches(L, world, rank)
 
-        def batched_fn(A_, B_, C_, alpha, beta):
-            return _bits_to_t(oracle.encode("f16", oracle.gemm_batched("f16", _t_to_bits(A_), _t_to_bits(B_))))
+        def batched_fn(A_, B_, C_, alpha, beta, out=None):
+            D = _bits_to_t(oracle.encode("f16", oracle.gemm_batched("f16", _t_to_bits(A_), _t_to_bits(B_))))
+            if out is not None:
+                out.copy_(D)
+                return out
+            return D
 
         Db = sharded_gemm_batched(_bits_to_t(A[s:e]), _bits_to_t(B[s:e]), L_total=L, replicate=True,
                                   batched_fn=batched_fn)
@@ -104,9 +108,14 @@ def _worker(rank, world, port, q):
         A, B0, B1, _, _ = synth.dual_inputs(300, 40, 64, seed=88, kind="int")
         s, e, _ = shard_rows(300, world, rank)
 
-        def dual_fn(A_, X, Y, a):
+        def dual_fn(A_, X, Y, a, out0=None, out1=None):
             r0, r1 = oracle.dual_gemm("f16", "pair", _t_to_bits(A_), _t_to_bits(X), _t_to_bits(Y), alpha=a)
-            return _bits_to_t(oracle.encode("f16", r0)), _bits_to_t(oracle.encode("f16", r1))
+            d0, d1 = _bits_to_t(oracle.encode("f16", r0)), _bits_to_t(oracle.encode("f16", r1))
+            if out0 is not None:
+                out0.copy_(d0)
+                out1.copy_(d1)
+                return out0, out1
+            return d0, d1
 
         d0, d1 = sharded_dual_gemm(_bits_to_t(A[s:e]), _bits_to_t(B0), _bits_to_t(B1), m_total=300, replicate=True,
                                    dual_fn=dual_fn)

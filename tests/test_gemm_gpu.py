@@ -170,6 +170,70 @@ def test_canary_padding_untouched():
     assert (full[:m, n:] == canary).all() and (full[m:, :] == canary).all()
 
 
+def test_rowreduce_n0_computes_y():
+    """Header contract: cy_gemm_rowreduce with n == 0 has no D tiles but still computes y = row sums
+    of A (stand-alone row-sum kernel, same fp32 k-order as the fused reducers: bit-identical to the
+    n > 0 path); k == 0 gives y = 0."""
+    for m, k in ((300, 200), (1, 7), (257, 1030)):
+        A, B, _ = synth.gemm_inputs(m, 64, k, seed=95 + m, kind="int")
+        dA = to_dev(A, "f16")
+        B0 = torch.empty((k, 0), dtype=torch.float16, device="cuda")
+        D, y = cy.gemm_rowreduce(dA, B0)
+        torch.cuda.synchronize()
+        assert D.shape == (m, 0)
+        assert np.array_equal(y.cpu().numpy().astype(np.float64), oracle.rowsum("f16", A))
+        Au, Bu, _ = synth.gemm_inputs(m, 64, k, seed=96 + m)
+        dAu = to_dev(Au, "f16")
+        _, y_fused = cy.gemm_rowreduce(dAu, to_dev(Bu, "f16"))
+        _, y_alone = cy.gemm_rowreduce(dAu, torch.empty((k, 0), dtype=torch.float16, device="cuda"))
+        torch.cuda.synchronize()
+        assert torch.equal(y_fused, y_alone), "n == 0 row sums differ from the fused reducers"
+    A0 = torch.empty((40, 0), dtype=torch.float16, device="cuda")
+    _, y0 = cy.gemm_rowreduce(A0, torch.empty((0, 0), dtype=torch.float16, device="cuda"))
+    torch.cuda.synchronize()
+    assert not y0.any()
+
+
+def test_binding_rejects_mismatched_operands():
+    """The torch binding checks what the C ABI cannot see (it gets only pointers and ld): dtypes,
+    C / out / y shapes, batched B shape, attention K/V shapes."""
+    f16 = dict(dtype=torch.float16, device="cuda")
+    A, B = torch.zeros((64, 32), **f16), torch.zeros((32, 48), **f16)
+    bad = [
+        lambda: cy.gemm(A, B.to(torch.bfloat16)),
+        lambda: cy.gemm(A, B, out=torch.zeros((64, 48), dtype=torch.float32, device="cuda")),
+        lambda: cy.gemm(A, B, C=torch.zeros((1, 48), **f16), beta=1.0),
+        lambda: cy.gemm(A, B, out=torch.zeros((32, 48), **f16)),
+        lambda: cy.gemm(A, B, beta=1.0),
+        lambda: cy.gemm(A, torch.zeros((16, 48), **f16)),
+        lambda: cy.gemm_batched(torch.zeros((2, 64, 32), **f16), torch.zeros((3, 32, 48), **f16)),
+        lambda: cy.gemm_batched(torch.zeros((2, 64, 32), **f16), torch.zeros((2, 16, 48), **f16)),
+        lambda: cy.dual_gemm(A, B, torch.zeros((32, 40), **f16)),
+        lambda: cy.gemm_rowreduce(A, B, y=torch.zeros((63,), dtype=torch.float32, device="cuda")),
+        lambda: cy.dual_gemm_glu(A, B, B, out=torch.zeros((64, 40), **f16)),
+        lambda: cy.attention(torch.zeros((1, 4, 128, 128), **f16), torch.zeros((1, 2, 128, 128), **f16),
+                             torch.zeros((1, 2, 128, 128), **f16)),
+        lambda: cy.attention(torch.zeros((1, 2, 128, 128), **f16), torch.zeros((1, 2, 128, 128), **f16),
+                             torch.zeros((1, 2, 64, 128), **f16)),
+        lambda: cy.attention(torch.zeros((1, 2, 128, 128), **f16), torch.zeros((1, 2, 128, 128), **f16),
+                             torch.zeros((1, 2, 128, 128), dtype=torch.bfloat16, device="cuda")),
+    ]
+    for i, fn in enumerate(bad):
+        with pytest.raises(ValueError):
+            fn()
+            pytest.fail(f"case {i} accepted")
+
+
+def test_binding_keeps_callers_device():
+    """A call on tensors of the current device leaves torch's current device alone (the binding
+    switches devices only for the call and restores the caller's)."""
+    before = torch.cuda.current_device()
+    A, B = torch.zeros((64, 32), dtype=torch.float16, device="cuda"), torch.zeros((32, 48), dtype=torch.float16,
+                                                                                    device="cuda")
+    cy.gemm(A, B)
+    assert torch.cuda.current_device() == before
+
+
 def test_misaligned_ld_rejected():
     A = torch.zeros((16, 12), dtype=torch.float16, device="cuda")
     B = torch.zeros((12, 16), dtype=torch.float16, device="cuda")
