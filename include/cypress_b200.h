@@ -39,6 +39,7 @@
 #ifndef CYPRESS_B200_H_
 #define CYPRESS_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -77,6 +78,29 @@ cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int6
                             const void* B, int64_t ldb, int64_t strideB, float beta,
                             const void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
                             int64_t strideD, void* stream);
+
+/* Split-K GEMM: the strided-batched GEMM of cy_gemm_batched with the K dimension of
+ * every output tile divided among `splits` work units, so that shapes with few output tiles and a
+ * long K (wave-quantised: the paper's small-size overheads) occupy every SM.  Each
+ * split accumulates its k-range in TMEM and writes an fp32 partial slice to `workspace`; the split
+ * that finishes a tile last sums the tile's partials in split order (deterministic, independent of
+ * arrival order; integer-valued inputs stay exact) and runs the usual epilogue (alpha, beta*C,
+ * one RN cast).  splits = 0: the library's cost model picks the count (1 = no split, the
+ * cy_gemm_batched kernel); splits = S >= 1: S (reduced to the largest count that leaves no split
+ * empty).  workspace: device memory of at least cy_gemm_splitk_workspace_size() bytes for the same
+ * arguments, 16-byte aligned, any contents (the arrival counters carry a per-launch tag, so stale
+ * bytes never count); it may be reused by later calls on the same stream, with any shape, but not by
+ * concurrent calls.  It must not overlap A, B, C or D.  Errors as cy_gemm_batched, plus CY_ERR_INVALID_VALUE for splits
+ * outside 0..64 or a workspace smaller than a requested split needs, CY_ERR_MISALIGNED for a
+ * misaligned workspace. */
+cy_status_t cy_gemm_splitk(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float alpha,
+                           const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                           int64_t strideB, float beta, const void* C, int64_t ldc, int64_t strideC, void* D,
+                           int64_t ldd, int64_t strideD, int splits, void* workspace, size_t workspace_bytes,
+                           void* stream);
+/* Workspace bytes cy_gemm_splitk needs for these arguments on the current device (0 when the
+ * choice is not to split, or the arguments are invalid). */
+size_t cy_gemm_splitk_workspace_size(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, int splits);
 
 /* Dual GEMM: A*B0 and A*B1 in one kernel sharing the A tiles, B0/B1 copies
  * overlapped in the main loop.  See cy_dual_mode_t. */
@@ -173,6 +197,8 @@ int cy_last_config(void);
  * bytes, dtype.  Any pointer may be NULL.  CY_ERR_INVALID_VALUE if nothing was launched yet. */
 cy_status_t cy_last_kernel_info(int* variant, int* cta_group, int* tile_m, int* tile_n, int* stages,
                                 int* threads, int* smem_bytes, int* dtype);
+/* Split count of the most recent successful GEMM-family launch (1 = not split). */
+int cy_last_splits(void);
 /* Number of kernel launches this library issued in this process (monotone counter). */
 int64_t cy_launch_count(void);
 

@@ -22,7 +22,7 @@ from ._lib import CY_BF16, CY_DUAL_PAIR, CY_DUAL_SUM, CY_F16, CyError, check
 
 __all__ = [
     "gemm", "gemm_batched", "dual_gemm", "dual_gemm_glu", "gemm_rowreduce", "gemm_replicated", "attention", "CyError", "force_config", "last_config",
-    "num_configs", "config_info", "launch_count", "last_kernel_info", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
+    "num_configs", "config_info", "launch_count", "last_kernel_info", "last_splits", "cy_gemm", "cy_gemm_batched", "cy_dual_gemm",
     "cy_gemm_rowreduce", "CY_F16", "CY_BF16", "CY_DUAL_PAIR", "CY_DUAL_SUM",
 ]
 
@@ -137,8 +137,58 @@ def _mat2(A, B):
     return m, B.shape[1], k
 
 
-def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
-    """D = alpha*A@B + beta*C  (A: m x k, B: k x n, row-major).  cy_gemm."""
+_WS = {}        # (device, stream) -> split-K workspace (uint8 tensor)
+_WS_NEED = {}   # (dtype, m, n, k, batch, splits, device, forced config) -> workspace bytes (0: not split)
+
+
+_FORCED = [-1]  # the config forced through force_config() (part of the workspace-size cache key)
+
+
+def _splitk_need(dt, m, n, k, L, splits, dev):
+    key = (dt, m, n, k, L, splits, dev, _FORCED[0])
+    need = _WS_NEED.get(key)
+    if need is None:
+        with _on_device(dev):
+            need = int(_lib.load().cy_gemm_splitk_workspace_size(dt, m, n, k, L, splits))
+        _WS_NEED[key] = need
+    return need
+
+
+def _workspace(dev, stream_handle, nbytes):
+    """Split-K workspace for (device, stream): calls on one stream reuse it (stream order; the
+    kernel's arrival counters are tagged per launch, so no zero fill); other streams get their own."""
+    torch = _torch()
+    key = (dev, int(stream_handle or 0))
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty((max(nbytes, 1 << 20),), dtype=torch.uint8, device=torch.device("cuda", dev))
+        _WS[key] = ws
+    return ws
+
+
+def _gemm_call(dt, m, n, k, L, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc, D, ldd, sd, stream, dev, splits,
+               what):
+    """cy_gemm_batched, or cy_gemm_splitk when split-K is requested (splits > 1) or chosen by the
+    library's cost model (splits=None: auto; the choice per shape is cached)."""
+    lib = _lib.load()
+    sk = 0 if splits is None else int(splits)
+    need = 0 if sk == 1 else _splitk_need(dt, m, n, k, L, sk, dev)
+    if need == 0 and sk <= 1 and L == 1 and sa == sb == sc == sd == 0:
+        st = lib.cy_gemm(dt, m, n, k, float(alpha), A, lda, B, ldb, float(beta), C, ldc, D, ldd, stream)
+    elif need == 0 and sk <= 1:
+        st = lib.cy_gemm_batched(dt, m, n, k, L, float(alpha), A, lda, sa, B, ldb, sb, float(beta), C, ldc, sc, D,
+                                 ldd, sd, stream)
+    else:
+        ws = _workspace(dev, stream, need)
+        st = lib.cy_gemm_splitk(dt, m, n, k, L, float(alpha), A, lda, sa, B, ldb, sb, float(beta), C, ldc, sc, D, ldd,
+                                sd, sk, ws.data_ptr(), ws.numel(), stream)
+    check(st, what)
+
+
+def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None, splits=None):
+    """D = alpha*A@B + beta*C  (A: m x k, B: k x n, row-major).  cy_gemm / cy_gemm_splitk.
+    splits: None = the library's choice (split-K only where its cost model predicts a gain),
+    1 = never split, S > 1 = split K into S parts."""
     dev = _check_dev(A, B, C, out)
     m, n, k = _mat2(A, B)
     use_c = beta != 0
@@ -150,14 +200,13 @@ def gemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=N
     if out is None:
         out = _empty2d(m, n, A)
     with _on_device(dev):
-        st = _lib.load().cy_gemm(_dt(A), m, n, k, float(alpha), _ptr(A), _ld(A, "A"), _ptr(B), _ld(B, "B"),
-                                 float(beta), _ptr(C) if use_c else None, _ld(C, "C") if use_c else n, _ptr(out),
-                                 _ld(out, "out"), _stream(stream, dev))
-    check(st, "cy_gemm")
+        _gemm_call(_dt(A), m, n, k, 1, alpha, _ptr(A), _ld(A, "A"), 0, _ptr(B), _ld(B, "B"), 0, beta,
+                   _ptr(C) if use_c else None, _ld(C, "C") if use_c else n, 0, _ptr(out), _ld(out, "out"), 0,
+                   _stream(stream, dev), dev, splits, "cy_gemm")
     return out
 
 
-def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):
+def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None, splits=None):
     """D[b] = alpha*A[b]@B[b] + beta*C[b] for b < L (3-D tensors, rows contiguous)."""
     torch = _torch()
     dev = _check_dev(A, B, C, out)
@@ -188,10 +237,8 @@ def gemm_batched(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None, 
     ldc, sc = lds(C if use_c else None)
     ldd, sd = lds(out)
     with _on_device(dev):
-        st = _lib.load().cy_gemm_batched(_dt(A), m, n, k, L, float(alpha), _ptr(A), lda, sa, _ptr(B), ldb, sb,
-                                         float(beta), _ptr(C) if use_c else None, ldc, sc, _ptr(out), ldd, sd,
-                                         _stream(stream, dev))
-    check(st, "cy_gemm_batched")
+        _gemm_call(_dt(A), m, n, k, L, alpha, _ptr(A), lda, sa, _ptr(B), ldb, sb, beta, _ptr(C) if use_c else None,
+                   ldc, sc, _ptr(out), ldd, sd, _stream(stream, dev), dev, splits, "cy_gemm_batched")
     return out
 
 
@@ -352,6 +399,7 @@ def gemm_rowreduce(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, out=None
 
 def force_config(cfg_id: int):
     check(_lib.load().cy_force_config(int(cfg_id)), "cy_force_config")
+    _FORCED[0] = int(cfg_id)
 
 
 def last_config() -> int:
@@ -384,6 +432,11 @@ def last_kernel_info() -> dict:
     d["variant"] = VARIANTS.get(d["variant"], d["variant"])
     d["dtype"] = "f16" if d["dtype"] == 0 else "bf16"
     return d
+
+
+def last_splits() -> int:
+    """Split count of the most recent GEMM-family launch (1 = not split)."""
+    return int(_lib.load().cy_last_splits())
 
 
 def launch_count() -> int:

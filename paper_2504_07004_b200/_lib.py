@@ -17,7 +17,8 @@ _PRODUCT_PATH = LIB_PATH
 EXPORTS = (
     "cy_gemm", "cy_gemm_batched", "cy_dual_gemm", "cy_dual_gemm_glu", "cy_gemm_rowreduce", "cy_status_string",
     "cy_num_configs", "cy_config_info", "cy_force_config", "cy_last_config", "cy_launch_count",
-    "cy_last_kernel_info", "cy_gemm_replicated", "cy_attention_fwd", "cy_peer_barrier",
+    "cy_last_kernel_info", "cy_gemm_replicated", "cy_attention_fwd", "cy_peer_barrier", "cy_gemm_splitk",
+    "cy_gemm_splitk_workspace_size", "cy_last_splits",
 )
 
 CY_OK = 0
@@ -58,6 +59,13 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     i64, f32, vp, ci = ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_int
     lib.cy_gemm.argtypes = [ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, i64, vp]
+    if hasattr(lib, "cy_gemm_splitk"):
+        lib.cy_gemm_splitk.argtypes = [ci, i64, i64, i64, i64, f32, vp, i64, i64, vp, i64, i64, f32, vp, i64, i64,
+                                       vp, i64, i64, ci, vp, ctypes.c_size_t, vp]
+        lib.cy_gemm_splitk.restype = ci
+        lib.cy_gemm_splitk_workspace_size.argtypes = [ci, i64, i64, i64, i64, ci]
+        lib.cy_gemm_splitk_workspace_size.restype = ctypes.c_size_t
+        lib.cy_last_splits.restype = ci
     lib.cy_gemm_batched.argtypes = [ci, i64, i64, i64, i64, f32, vp, i64, i64, vp, i64, i64, f32,
                                     vp, i64, i64, vp, i64, i64, vp]
     lib.cy_dual_gemm.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, vp, i64, f32, vp, i64,

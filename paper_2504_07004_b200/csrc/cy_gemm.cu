@@ -109,6 +109,7 @@ const int g_a_reuse = [] {
   return e ? std::atoi(e) : 1;
 }();
 std::atomic<int> g_last{-1};
+std::atomic<int> g_last_splits{1};
 std::atomic<int64_t> g_launches{0};
 
 // ------------------------------------------------------------------------------------------
@@ -233,10 +234,10 @@ bool overlap(Range a, Range b) { return a.lo < a.hi && b.lo < b.hi && a.lo < b.h
 
 // ------------------------------------------------------------------------------------------
 // config choice: minimise (waves x tile area / efficiency)
-double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k, int64_t L, int sms) {
+double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k, int64_t L, int sms, int splits = 1) {
   // time ~ waves x (tile area per SM) x (K + exposed epilogue) / efficiency
   const int64_t bm = 128 * cg;
-  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
+  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn) * splits;
   const int64_t units = sms / cg;
   const int64_t waves = (tiles + units - 1) / units;
   // relative per-SM efficiency of each tile shape, measured on B200 at 8192^3 under the power cap
@@ -247,33 +248,80 @@ double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k,
   if (cg == 1 && bn == 256) eff = 0.80;
   if (cg == 1 && bn == 128) eff = 0.60;
   if (cg == 1 && bn == 64) eff = 0.40;
-  const double kk = static_cast<double>(std::max<int64_t>(k, 64)) + (single_buf ? 128.0 : 0.0) + 128.0;
+  const int64_t kb = (k + 63) / 64;
+  const int64_t kb_split = (kb + splits - 1) / splits;
+  double kk = static_cast<double>(std::max<int64_t>(kb_split * 64, 64)) + (single_buf ? 128.0 : 0.0) + 128.0;
+  // split-K: every split writes its 128 x bn fp32 partial per CTA (~8 bn cycles at ~64 B/clk of
+  // L2 bandwidth) and the last one reads all `splits` partials back; one k-block costs 2 bn cycles
+  // per SM, so the reduction weighs (splits + 1) * 4 k-blocks = (splits + 1) * 256 K elements
+  if (splits > 1) kk += (splits + 1) * 256.0;
   return static_cast<double>(waves) * static_cast<double>(bm * bn) / cg * kk / eff;
 }
 
-int pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms) {
+// Menu entry and split count: the smallest predicted time.  max_splits > 1 lets split-K (V_GEMM
+// with one accumulator per tile) compete; ws_bytes bounds the workspace a split may use.
+struct Choice {
+  int idx = -1, splits = 1;
+};
+size_t splitk_ws_bytes(const KDesc& kd, int64_t m, int64_t n, int64_t L, int splits);
+
+Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms, int max_splits = 1,
+            size_t ws_bytes = 0, int forced_splits = 0, bool use_forced = true) {
   const auto& mn = menu();
-  int forced = g_forced.load();
-  if (forced >= 0 && forced < kNumGemmCfg) {
-    for (size_t i = 0; i < mn.size(); ++i)
-      if (mn[i].var == var && mn[i].dt == dt && mn[i].cg == kGemmMenu[forced].cg &&
-          mn[i].bn == kGemmMenu[forced].bn && mn[i].mc == kGemmMenu[forced].mc)
-        return static_cast<int>(i);
-  }
-  int best = -1;
+  Choice best;
   double best_cost = 0;
+  const int64_t kb = (k + 63) / 64;
+  const int forced = use_forced ? g_forced.load() : -1;
+  // splits that leave no split empty: S -> ceil(kb / ceil(kb / S))
+  auto eff_splits = [&](int sp) {
+    if (kb <= 1 || sp <= 1) return 1;
+    const int64_t kbs = (kb + sp - 1) / sp;
+    return static_cast<int>((kb + kbs - 1) / kbs);
+  };
   for (size_t i = 0; i < mn.size(); ++i) {
     if (mn[i].var != var || mn[i].dt != dt) continue;
-    if (mn[i].mc != 1) continue;  // B-multicast clusters: only when forced (being evaluated)
-    const bool dual = (var == cy::V_DUAL_PAIR || var == cy::V_DUAL_SUM || var == cy::V_DUAL_GLU);
+    if (forced >= 0 && forced < kNumGemmCfg) {
+      if (!(mn[i].cg == kGemmMenu[forced].cg && mn[i].bn == kGemmMenu[forced].bn && mn[i].mc == kGemmMenu[forced].mc))
+        continue;
+    } else if (mn[i].mc != 1) {
+      continue;  // B-multicast clusters: only when forced (being evaluated)
+    }
     const int acc_cols = ((var == cy::V_DUAL_PAIR || var == cy::V_DUAL_GLU) ? 2 : 1) * mn[i].bn;
-    (void)dual;
     const int single = acc_cols * 2 > 512;
-    double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, sms);
-
-    if (best < 0 || c < best_cost) { best = static_cast<int>(i); best_cost = c; }
+    const bool can_split = var == cy::V_GEMM && mn[i].mc == 1 && mn[i].bn <= 256;  // one accumulator (NSUB 1)
+    if (!can_split && forced_splits > 1) continue;  // a requested split needs a splittable kernel
+    const int s_hi = can_split ? static_cast<int>(std::min<int64_t>(max_splits, std::max<int64_t>(kb, 1))) : 1;
+    for (int sp = 1; sp <= s_hi; ++sp) {
+      if (eff_splits(sp) != sp) continue;  // same k-block ranges as a smaller count
+      if (can_split && forced_splits > 0 && sp != eff_splits(std::min(forced_splits, s_hi))) continue;
+      if (sp > 1 && splitk_ws_bytes(mn[i], m, n, L, sp) > ws_bytes) continue;
+      const double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, sms, sp);
+      if (best.idx < 0 || c < best_cost) {
+        best.idx = static_cast<int>(i);
+        best.splits = sp;
+        best_cost = c;
+      }
+    }
   }
+  if (best.idx < 0 && forced >= 0)  // the forced shape has no kernel of this variant: heuristic
+    return pick(var, dt, m, n, k, L, sms, max_splits, ws_bytes, forced_splits, false);
   return best;
+}
+
+// Split-K workspace: [counters: one 64-bit epoch-tagged count per (tile, CTA, epilogue warp), padded
+// to 256 B]
+// [partials: tiles x CTAs x 128 rows x TILE_N fp32 per split].
+size_t splitk_counter_bytes(const KDesc& kd, int64_t m, int64_t n, int64_t L) {
+  const int64_t bm = 128 * kd.cg * kd.mc;
+  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + kd.bn - 1) / kd.bn);
+  const int epi_warps = kd.threads / 32 - 2;  // V_GEMM: producer + MMA + epilogue warps
+  return static_cast<size_t>((tiles * kd.cg * epi_warps * 8 + 255) / 256 * 256);
+}
+size_t splitk_ws_bytes(const KDesc& kd, int64_t m, int64_t n, int64_t L, int splits) {
+  if (splits <= 1) return 0;
+  const int64_t bm = 128 * kd.cg * kd.mc;
+  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + kd.bn - 1) / kd.bn);
+  return splitk_counter_bytes(kd, m, n, L) + static_cast<size_t>(tiles * kd.cg * 128 * kd.bn * 4) * splits;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -284,13 +332,15 @@ struct Operand {
 
 cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, float alpha, Operand A,
                    Operand B0, Operand B1, float beta, Operand C0, Operand C1, Operand D0, Operand D1, float* y,
-                   void* stream, int act = 0, const Operand* extra_dst = nullptr, int n_extra = 0) {
+                   void* stream, int act = 0, const Operand* extra_dst = nullptr, int n_extra = 0, int max_splits = 1,
+                   void* ws = nullptr, size_t ws_bytes = 0, int forced_splits = 0) {
   int dev;
   DevState* st;
   cy_status_t s = device_state(dev, st);
   if (s != CY_OK) return s;
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX || L > INT32_MAX) return CY_ERR_INVALID_VALUE;
-  const int idx = pick(var, dt, m, n, k, L, st->sms);
+  const Choice ch = pick(var, dt, m, n, k, L, st->sms, max_splits, ws_bytes, forced_splits);
+  const int idx = ch.idx;
   if (idx < 0) return CY_ERR_INTERNAL;
   const KDesc& kd = menu()[idx];
   const int bm = 128 * kd.cg * kd.mc;  // rows per cluster tile
@@ -329,8 +379,22 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.m_blocks = (int)((m + bm - 1) / bm);
   p.n_blocks = (int)((n + kd.bn - 1) / kd.bn);
   p.k_blocks = (int)((k + 63) / 64);
-  p.tiles = (int)(L * p.m_blocks * p.n_blocks);
-  p.group_m = g_group_m > 0 ? g_group_m : 8;
+  p.splits = ch.splits;
+  p.kb_split = p.splits > 1 ? (p.k_blocks + p.splits - 1) / p.splits : p.k_blocks;
+  p.ws = nullptr;
+  p.ws_cnt = nullptr;
+  p.epoch = 0;
+  if (p.splits > 1) {
+    static std::atomic<unsigned int> g_epoch{0};
+    unsigned int e = g_epoch.fetch_add(1) + 1;
+    if (e == 0) e = g_epoch.fetch_add(1) + 1;  // 0 is never a launch tag
+    p.epoch = e;
+    p.ws_cnt = static_cast<unsigned long long*>(ws);
+    p.ws = reinterpret_cast<float*>(static_cast<char*>(ws) + splitk_counter_bytes(kd, m, n, L));
+  }
+  if (L * p.m_blocks * p.n_blocks * p.splits > INT32_MAX) return CY_ERR_INVALID_VALUE;
+  p.tiles = (int)(L * p.m_blocks * p.n_blocks * p.splits);
+  p.group_m = g_group_m > 0 ? g_group_m : 12;  // measured 8192^3 / 65536x8192^2: 6 8 12 16 24 -> 12 best (profiles/r02_group_m.md)
   p.l2_policy = g_l2_policy;
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
@@ -403,6 +467,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
     return CY_ERR_LAUNCH;
   }
   g_last.store(idx);
+  g_last_splits.store(p.splits);
   g_launches.fetch_add(1);
   return CY_OK;
 }
@@ -526,10 +591,10 @@ static cy_status_t check_common(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, 
   return CY_OK;
 }
 
-cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float alpha,
-                            const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
-                            int64_t strideB, float beta, const void* C, int64_t ldc, int64_t strideC, void* D,
-                            int64_t ldd, int64_t strideD, void* stream) {
+static cy_status_t check_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float beta,
+                                 const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                                 int64_t strideB, const void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
+                                 int64_t strideD) {
   cy_status_t s = check_common(dt, m, n, k, batch);
   if (s != CY_OK) return s;
   if (m == 0 || n == 0 || batch == 0) return CY_OK;
@@ -550,9 +615,70 @@ cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int6
     return CY_ERR_INVALID_VALUE;
   if (has_c && !(C == D && ldc == ldd && strideC == strideD) && overlap(rD, span(C, m, n, ldc, batch, strideC, 2)))
     return CY_ERR_INVALID_VALUE;
+  return CY_OK;
+}
+
+cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float alpha,
+                            const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                            int64_t strideB, float beta, const void* C, int64_t ldc, int64_t strideC, void* D,
+                            int64_t ldd, int64_t strideD, void* stream) {
+  cy_status_t s = check_batched(dt, m, n, k, batch, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, D, ldd,
+                                strideD);
+  if (s != CY_OK || m == 0 || n == 0 || batch == 0) return s;
   return launch(cy::V_GEMM, dt, m, n, k, batch, alpha, {A, lda, strideA}, {B, ldb, strideB}, {nullptr, 0, 0}, beta,
                 {C, ldc, strideC}, {nullptr, 0, 0}, {D, ldd, strideD}, {nullptr, 0, 0}, nullptr, stream);
 }
+
+// split-K: the choice the library makes for (shape, splits) with an unbounded workspace
+static constexpr int kMaxAutoSplits = 16;
+static Choice splitk_choice(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, int splits, int sms) {
+  return pick(cy::V_GEMM, dt, m, n, k, batch, sms, splits == 0 ? kMaxAutoSplits : splits, SIZE_MAX, splits);
+}
+
+size_t cy_gemm_splitk_workspace_size(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, int splits) {
+  if (check_common(dt, m, n, k, batch) != CY_OK || splits < 0 || splits > 64 || m == 0 || n == 0 || batch == 0)
+    return 0;
+  int dev;
+  DevState* st;
+  if (device_state(dev, st) != CY_OK) return 0;
+  const Choice ch = splitk_choice(dt, m, n, k, batch, splits, st->sms);
+  if (ch.idx < 0) return 0;
+  return splitk_ws_bytes(menu()[ch.idx], m, n, batch, ch.splits);
+}
+
+cy_status_t cy_gemm_splitk(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float alpha,
+                           const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb, int64_t strideB,
+                           float beta, const void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
+                           int64_t strideD, int splits, void* workspace, size_t workspace_bytes, void* stream) {
+  if (splits < 0 || splits > 64) return CY_ERR_INVALID_VALUE;
+  cy_status_t s = check_batched(dt, m, n, k, batch, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, D, ldd,
+                                strideD);
+  if (s != CY_OK || m == 0 || n == 0 || batch == 0) return s;
+  if (workspace_bytes > 0 && !workspace) return CY_ERR_INVALID_VALUE;
+  if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 15u)) return CY_ERR_MISALIGNED;
+  if (workspace && workspace_bytes > 0) {
+    const Range rW{reinterpret_cast<uintptr_t>(workspace), reinterpret_cast<uintptr_t>(workspace) + workspace_bytes};
+    const bool has_c = beta != 0.0f;
+    if (overlap(rW, span(D, m, n, ldd, batch, strideD, 2)) ||
+        (k > 0 && (overlap(rW, span(A, m, k, lda, batch, strideA, 2)) || overlap(rW, span(B, k, n, ldb, batch, strideB, 2)))) ||
+        (has_c && overlap(rW, span(C, m, n, ldc, batch, strideC, 2))))
+      return CY_ERR_INVALID_VALUE;
+  }
+  if (splits > 1) {  // a requested split count must fit the workspace it was given
+    int dev;
+    DevState* st;
+    s = device_state(dev, st);
+    if (s != CY_OK) return s;
+    const Choice ch = splitk_choice(dt, m, n, k, batch, splits, st->sms);
+    if (ch.idx >= 0 && splitk_ws_bytes(menu()[ch.idx], m, n, batch, ch.splits) > workspace_bytes)
+      return CY_ERR_INVALID_VALUE;
+  }
+  return launch(cy::V_GEMM, dt, m, n, k, batch, alpha, {A, lda, strideA}, {B, ldb, strideB}, {nullptr, 0, 0}, beta,
+                {C, ldc, strideC}, {nullptr, 0, 0}, {D, ldd, strideD}, {nullptr, 0, 0}, nullptr, stream, 0, nullptr, 0,
+                splits == 0 ? kMaxAutoSplits : splits, workspace, workspace_bytes, splits);
+}
+
+int cy_last_splits(void) { return g_last_splits.load(); }
 
 cy_status_t cy_gemm(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, float alpha, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float beta, const void* C, int64_t ldc, void* D, int64_t ldd,

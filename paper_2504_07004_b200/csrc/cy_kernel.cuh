@@ -50,7 +50,7 @@ struct Params {
   float alpha, beta;
   int has_c;             // beta != 0: C is read
   int m_blocks, n_blocks, k_blocks;
-  int tiles;             // L * m_blocks * n_blocks
+  int tiles;             // work units: L * m_blocks * n_blocks * splits
   int group_m;           // grouped rasterisation width (in m-blocks)
   int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
@@ -58,6 +58,11 @@ struct Params {
   int n_extra;           // number of extra D destinations in DstMaps (0 = D only)
   int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
   int sleep_ns;          // >0: epilogue waits for the accumulator with nanosleep backoff (cap, ns)
+  int splits;            // split-K (V_GEMM): work unit u = tile u / splits, k-blocks of split u % splits
+  int kb_split;          // k-blocks per split (the last split may hold fewer; every split holds >= 1)
+  float* ws;             // split-K: fp32 partial slices (cy_gemm_splitk workspace)
+  unsigned long long* ws_cnt;  // split-K: per-slice arrival counters, (launch epoch << 32) | arrivals
+  unsigned int epoch;    // split-K: this launch's tag (non-zero, different from the previous launches')
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride;
                          // 2: one cluster per tile, no stealing (non-persistent)
@@ -149,6 +154,14 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& b, int&
   const int rg = r - g * group;
   mb = first_m + rg % gm;
   nb = rg / gm;
+}
+
+// Work unit u (split-K: tile u / splits, k-block range of split u % splits).
+__device__ __forceinline__ void unit_coords(const Params& p, int u, int& b, int& mb, int& nb, int& kb0, int& kb1) {
+  const int tile = u / p.splits;
+  tile_coords(p, tile, b, mb, nb);
+  kb0 = (u - tile * p.splits) * p.kb_split;
+  kb1 = min(p.k_blocks, kb0 + p.kb_split);
 }
 
 // GLU activations in fp32 (reading R14): SiLU x / (1 + e^-x); GELU tanh form
@@ -308,11 +321,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int t;
       for (int i = 0; sched_next(i, t, false); ++i) {
         sched_request(i);
-        int b, mb, nb;
-        tile_coords(p, t, b, mb, nb);
+        int b, mb, nb, kb0, kb1;
+        unit_coords(p, t, b, mb, nb, kb0, kb1);
         const int am = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA;
         const int bn = nb * C::TILE_N + rank * C::BN_CTA;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(bEmpty + 8 * stage, phase ^ 1);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
@@ -366,6 +379,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       uint32_t stage = 0, phase = 0;
       constexpr uint16_t kAllMask = uint16_t((1u << C::CL) - 1u);  // stage release: every CTA of the cluster
       const uint16_t pair_mask = uint16_t(0x3u << leader);          // this pair's two CTAs
+      int kfirst = 0;  // first k-block of the current work unit (accumulate = 0 there)
       // all 4 k16 MMAs of one k-block for B slot `sl` of ring stage `st` into accumulator base `d`
       auto issue = [&](uint32_t d, int st, int sl, int kb) {
         const uint32_t sA = sStage0 + st * C::STAGE_BYTES;
@@ -377,7 +391,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           // B: MN-major SW128, 64-column atoms B_ATOM_BYTES apart (LBO), 8-K-row groups 1024 B
           // apart (SBO); K advances 16 rows = 2048 B.
           const uint64_t bd = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
-          const uint32_t acc = (kb | kk) != 0;
+          const uint32_t acc = (kb != kfirst || kk != 0);
           if constexpr (C::VAR == V_DUAL_SUM) mma_f16<C::CG>(d, ad, bd, C::IDESC, sl ? 1u : acc);
           else mma_f16<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
         }
@@ -392,7 +406,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
           const uint64_t bd0 = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
           const uint64_t bd1 = sdesc_sw128(sB + C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
-          const uint32_t acc = (kb | kk) != 0;
+          const uint32_t acc = (kb != kfirst || kk != 0);
           if constexpr (C::VAR == V_DUAL_SUM) {
             mma_f16_col<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
             mma_f16_col<C::CG, 2>(d, ad, bd1, C::IDESC, 1u);
@@ -411,10 +425,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
         const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
         const uint32_t d = tmem_base + buf * C::ACC_COLS;
+        int ub, umb, unb, kb0, kb1;
+        unit_coords(p, t, ub, umb, unb, kb0, kb1);
+        kfirst = kb0;
         if constexpr (!C::SPLIT) {
           mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
           tc_fence_after();
-          for (int kb = 0; kb < p.k_blocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(bFull + 8 * stage, phase);
             tc_fence_after();
             if constexpr (C::NUM_B == 2) {
@@ -440,7 +457,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             }
             held = 0;
           };
-          for (int kb = 0; kb < p.k_blocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(bFull + 8 * stage, phase);
             tc_fence_after();
             if (acc1 && held == 0 && p.a_reuse) {  // steady state: both accumulators, A reused
@@ -514,13 +531,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     };
     int t;
+    // C prefetch: not with split-K (only the last-arriving split of a tile stores it)
+    const bool cpf = CPF && p.has_c && p.splits == 1;
     for (int it = 0; sched_next(it, t, true); ++it) {
-      int b, mb, nb;
-      tile_coords(p, t, b, mb, nb);
+      int b, mb, nb, kb0, kb1;
+      unit_coords(p, t, b, mb, nb, kb0, kb1);
+      const bool has_k = kb1 > kb0;
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
       const int row0 = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA + 32 * q4;
-      if (CPF && p.has_c) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
+      if (cpf) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
       if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
       else mbar_wait(bTFull + 8 * buf, bph);
       tc_fence_after();
@@ -554,7 +574,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       // wait until the current slot may be written (no C) / holds chunk q's C tile
       auto slot_ready = [&](int q) {
         if (p.has_c) {
-          if (!CPF) fetch_c(nb, row0, b, q, slot);
+          if (!cpf) fetch_c(nb, row0, b, q, slot);
           mbar_wait(cbar, cphase);
           cphase ^= 1;
         } else {
@@ -573,75 +593,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           bulk_commit();
         }
         if constexpr (C::EPI_BUFS == 2) slot ^= 1;
-        if (CPF && p.has_c && q + 1 < NQ) fetch_c(nb, row0, b, q + 1, slot);  // next chunk's C
+        if (cpf && q + 1 < NQ) fetch_c(nb, row0, b, q + 1, slot);  // next chunk's C
       };
       const bool unit_alpha = (p.alpha == 1.0f);
-      if (G == 2 && !p.has_c) {
-        // beta == 0, single-buffered TMEM: both of this warp's chunks of an accumulator are loaded
-        // and rounded (alpha*acc, one RN cast) into 16-bit pairs before the accumulator is handed
-        // back, so the MMA issuer waits only for the TMEM loads.
-#pragma unroll 1
-        for (int a = 0; a < C::NUM_OUT; ++a) {
-          uint32_t pk[2][32];
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            uint32_t r[64];
-            if (p.k_blocks > 0) {
-              const uint32_t ta = tmem_chunk(a, a * CPW + g);
-              tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-              tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-              tmem_ld_wait();
-            } else {
-#pragma unroll
-              for (int i = 0; i < 64; ++i) r[i] = 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-              pk[g][i] = unit_alpha ? pack2<C::DT>(x0, x1) : pack2<C::DT>(x0 * p.alpha, x1 * p.alpha);
-            }
-          }
-          release(a);
-          if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            slot_ready(a * CPW + g);
-            const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
-#pragma unroll
-            for (int v = 0; v < 8; ++v)
-              st_shared_v4(row_addr + ((v ^ (lane & 7)) << 4), pk[g][4 * v], pk[g][4 * v + 1], pk[g][4 * v + 2],
-                           pk[g][4 * v + 3]);
-            store_chunk(a * CPW + g);
-          }
-        }
-        continue;
-      }
-#pragma unroll 1
-      for (int q = 0; q < NQ; ++q) {
-        const int a = q / CPW;
-        uint32_t r[64];
-        uint32_t gt[C::GLU ? 64 : 1];  // GLU: the gate operand (accumulator 1)
-        if (p.k_blocks > 0) {
-          const uint32_t ta = tmem_chunk(a, q);
-          tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-          if constexpr (C::GLU) {
-            tmem_ld_32x32b_x32(ta + C::BN, *reinterpret_cast<uint32_t(*)[32]>(&gt[0]));
-            tmem_ld_32x32b_x32(ta + C::BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&gt[32]));
-          }
-          tmem_ld_wait();
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) r[i] = 0u;
-          if constexpr (C::GLU) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) gt[i] = 0u;
-          }
-        }
-        // The accumulator's last chunk is in registers: hand its TMEM columns back to the MMA
-        // issuer before converting and storing it.
-        if ((q + 1) % CPW == 0) release(a);
-        if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
+      // chunk q from fp32 registers (r: the accumulator, gt: GLU gate) -> alpha/act/beta*C in fp32
+      // -> one RN cast -> swizzled staging -> TMA store
+      auto emit = [&](int q, const uint32_t (&r)[64], const uint32_t (&gt)[C::GLU ? 64 : 1]) {
         slot_ready(q);
         const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
 #pragma unroll
@@ -673,6 +630,144 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                        pack2<C::DT>(f[6], f[7]));
         }
         store_chunk(q);
+      };
+      auto load_chunk = [&](int q, uint32_t (&r)[64], uint32_t (&gt)[C::GLU ? 64 : 1]) {
+        const int a = q / CPW;
+        if (has_k) {
+          const uint32_t ta = tmem_chunk(a, q);
+          tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          if constexpr (C::GLU) {
+            tmem_ld_32x32b_x32(ta + C::BN, *reinterpret_cast<uint32_t(*)[32]>(&gt[0]));
+            tmem_ld_32x32b_x32(ta + C::BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&gt[32]));
+          }
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) r[i] = 0u;
+          if constexpr (C::GLU) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) gt[i] = 0u;
+          }
+        }
+      };
+      if constexpr (C::VAR == V_GEMM && C::MC == 1 && C::NSUB == 1) {  // (the host splits only these)
+        if (p.splits > 1) {
+          // ---- split-K: every split of a tile writes its fp32 partial slice
+          // (this warp's 32 rows x NQ chunks) to the workspace and counts itself in; the split that
+          // arrives last sums all slices in split order (deterministic, independent of arrival
+          // order) and runs the normal epilogue.  Slice layout: float4 j of lane l of chunk q at
+          // ((q*16 + j)*32 + l): every warp-wide access is 512 contiguous bytes.
+          const int tile = t / p.splits, sp = t - tile * p.splits;
+          const int wslot = (tile * C::CG + int(rank)) * C::EPI_WARPS + ew;
+          constexpr int SLICE4 = NQ * 16 * 32;  // float4 per slice
+          float4* wsl = reinterpret_cast<float4*>(p.ws) + size_t(wslot) * p.splits * SLICE4;
+          uint32_t gt[C::GLU ? 64 : 1];
+#pragma unroll 1
+          for (int q = 0; q < NQ; ++q) {
+            uint32_t r[64];
+            load_chunk(q, r, gt);
+            if ((q + 1) % CPW == 0) release(q / CPW);
+            float4* dst = wsl + size_t(sp) * SLICE4 + q * 16 * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              __stcg(dst + 32 * j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+          }
+          __threadfence();
+          __syncwarp();
+          // arrivals before ours in this launch: a counter tagged with another launch's epoch (left by
+          // an earlier call, or workspace bytes an earlier call used otherwise) counts as zero, so the
+          // workspace needs no zero fill and no reset
+          int before = 0;
+          if (lane == 0) {
+            unsigned long long* cnt = p.ws_cnt + wslot;
+            unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(cnt), want;
+            do {
+              want = seen;
+              const bool mine = static_cast<unsigned int>(want >> 32) == p.epoch;
+              before = mine ? static_cast<int>(want & 0xffffffffull) : 0;
+              seen = atomicCAS(cnt, want, mine ? want + 1 : ((static_cast<unsigned long long>(p.epoch) << 32) | 1ull));
+            } while (seen != want);
+          }
+          before = __shfl_sync(0xffffffffu, before, 0);
+          if (before != p.splits - 1) continue;  // another split of this tile finishes it
+          __threadfence();
+#pragma unroll 1
+          for (int q = 0; q < NQ; ++q) {
+            uint32_t r[64];
+#pragma unroll 1
+            for (int s2 = 0; s2 < p.splits; ++s2) {
+              const float4* src = wsl + size_t(s2) * SLICE4 + q * 16 * 32 + lane;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float4 v = __ldcg(src + 32 * j);
+                if (s2 == 0) {
+                  r[4 * j] = __float_as_uint(v.x), r[4 * j + 1] = __float_as_uint(v.y);
+                  r[4 * j + 2] = __float_as_uint(v.z), r[4 * j + 3] = __float_as_uint(v.w);
+                } else {
+                  r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+                  r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+                  r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+                  r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+                }
+              }
+            }
+            emit(q, r, gt);
+          }
+          continue;
+        }
+      }
+      if (G == 2 && !p.has_c) {
+        // beta == 0, single-buffered TMEM: both of this warp's chunks of an accumulator are loaded
+        // and rounded (alpha*acc, one RN cast) into 16-bit pairs before the accumulator is handed
+        // back, so the MMA issuer waits only for the TMEM loads.
+#pragma unroll 1
+        for (int a = 0; a < C::NUM_OUT; ++a) {
+          uint32_t pk[2][32];
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            uint32_t r[64];
+            if (has_k) {
+              const uint32_t ta = tmem_chunk(a, a * CPW + g);
+              tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) r[i] = 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+              pk[g][i] = unit_alpha ? pack2<C::DT>(x0, x1) : pack2<C::DT>(x0 * p.alpha, x1 * p.alpha);
+            }
+          }
+          release(a);
+          if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            slot_ready(a * CPW + g);
+            const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              st_shared_v4(row_addr + ((v ^ (lane & 7)) << 4), pk[g][4 * v], pk[g][4 * v + 1], pk[g][4 * v + 2],
+                           pk[g][4 * v + 3]);
+            store_chunk(a * CPW + g);
+          }
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int q = 0; q < NQ; ++q) {
+        uint32_t r[64];
+        uint32_t gt[C::GLU ? 64 : 1];  // GLU: the gate operand (accumulator 1)
+        load_chunk(q, r, gt);
+        // The accumulator's last chunk is in registers: hand its TMEM columns back to the MMA
+        // issuer before converting and storing it.
+        if ((q + 1) % CPW == 0) release(q / CPW);
+        if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
+        emit(q, r, gt);
       }
     }
     if (lane == 0) bulk_wait_read<0>();  // shared staging must outlive the stores' reads

@@ -826,3 +826,88 @@ def test_bench_json_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 8192 * 8192 * 2 and e["d2h_bytes_per_step"] == 8192 * 8192 * 2
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+# ---------------------------------------------------------------- split-K
+SPLIT_SHAPES = [(256, 256, 1024), (300, 264, 1000), (129, 257, 4100), (1024, 512, 8192)]
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("splits", [2, 3, 4, 7])
+@pytest.mark.parametrize("shape", SPLIT_SHAPES)
+def test_splitk_integer_bit_exact(cfg, splits, shape):
+    """Split-K on every splittable config: integer inputs (partials < 2^24) give the one correct
+    result, RN(oracle), bit for bit, including alpha/beta*C and ragged k-block counts."""
+    m, n, k = shape
+    A, B, C = synth.gemm_inputs(m, n, k, seed=1300 + m + splits, kind="int", with_c=True)
+    cy.force_config(cfg)
+    D = cy.gemm(to_dev(A, "f16"), to_dev(B, "f16"), to_dev(C, "f16"), 2.0, -1.0, splits=splits)
+    torch.cuda.synchronize()
+    want_s = min(splits, (k + 63) // 64)
+    assert 1 < cy.last_splits() <= want_s
+    assert_bits_equal(to_bits(D), oracle.encode("f16", oracle.gemm("f16", A, B, C, 2.0, -1.0)),
+                      f"cfg{cfg} splits{splits} {shape}")
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_splitk_uniform_tolerance_and_deterministic(dtype):
+    m, n, k = 512, 384, 8192
+    A, B, _ = synth.gemm_inputs(m, n, k, seed=1401, dtype=dtype)
+    dA, dB = to_dev(A, dtype), to_dev(B, dtype)
+    D1 = to_bits(cy.gemm(dA, dB, splits=5))
+    D2 = to_bits(cy.gemm(dA, dB, splits=5))
+    assert_bits_equal(D1, D2, "split-K repeat (deterministic summation order)")
+    assert_within_tol(D1, oracle.gemm(dtype, A, B), k, dtype, what=f"split-K {dtype}")
+
+
+def test_splitk_batched_and_workspace_reuse():
+    """Batched split-K, and one workspace reused over calls of different shapes and split counts
+    (stale partials and counters from earlier calls never count: per-launch tags): every call gives
+    the exact result; also a workspace filled with garbage before the first call."""
+    ws = cy._WS.get((torch.cuda.current_device(), int(torch.cuda.current_stream().cuda_stream)))
+    if ws is not None:
+        ws.fill_(0x5A)
+    L, m, n, k = 6, 200, 136, 2048
+    A, B, C = synth.gemm_inputs(m, n, k, seed=1402, batch=L, kind="int", with_c=True)
+    dA, dB, dC = to_dev(A, "f16"), to_dev(B, "f16"), to_dev(C, "f16")
+    want = oracle.encode("f16", oracle.gemm_batched("f16", A, B, C, 1.0, 1.0))
+    for it in range(6):
+        D = cy.gemm_batched(dA, dB, dC, 1.0, 1.0, splits=2 + it % 3)
+        torch.cuda.synchronize()
+        assert_bits_equal(to_bits(D), want, f"batched split-K call {it}")
+
+
+def test_splitk_auto_choice():
+    """The cost model splits a long-K shape with few output tiles and leaves 8192^3 unsplit."""
+    A, B, _ = synth.gemm_inputs(1024, 1024, 16384, seed=1403, kind="int")
+    D = cy.gemm(to_dev(A, "f16"), to_dev(B, "f16"))
+    torch.cuda.synchronize()
+    assert cy.last_splits() > 1
+    assert_bits_equal(to_bits(D), oracle.encode("f16", oracle.gemm("f16", A, B)), "auto split-K")
+    lib = cy._lib.load()
+    assert lib.cy_gemm_splitk_workspace_size(0, 8192, 8192, 8192, 1, 0) == 0
+    x = torch.zeros((256, 256), dtype=torch.float16, device="cuda")
+    cy.gemm(x, x)
+    assert cy.last_splits() == 1
+
+
+def test_splitk_argument_errors():
+    import ctypes
+
+    lib = cy._lib.load()
+    A = torch.zeros((256, 4096), dtype=torch.float16, device="cuda")
+    B = torch.zeros((4096, 256), dtype=torch.float16, device="cuda")
+    D = torch.zeros((256, 256), dtype=torch.float16, device="cuda")
+    ws = torch.zeros((1 << 24,), dtype=torch.uint8, device="cuda")
+    args = lambda sp, w, nb: (0, 256, 256, 4096, 1, 1.0, A.data_ptr(), 4096, 0, B.data_ptr(), 256, 0, 0.0, None, 256,  # noqa
+                              0, D.data_ptr(), 256, 0, sp, w, nb, None)
+    assert lib.cy_gemm_splitk(*args(65, ws.data_ptr(), ws.numel())) == 1
+    assert lib.cy_gemm_splitk(*args(-1, ws.data_ptr(), ws.numel())) == 1
+    assert lib.cy_gemm_splitk(*args(4, ws.data_ptr() + 4, ws.numel() - 4)) == 2
+    assert lib.cy_gemm_splitk(*args(4, ws.data_ptr(), 1024)) == 1  # too small for 4 splits
+    assert lib.cy_gemm_splitk(*args(4, D.data_ptr(), D.numel() * 2)) == 1  # overlaps D
+    need = lib.cy_gemm_splitk_workspace_size(0, 256, 256, 4096, 1, 4)
+    assert 0 < need <= ws.numel()
+    assert lib.cy_gemm_splitk(*args(4, ws.data_ptr(), need)) == 0
+    torch.cuda.synchronize()
+    del ctypes
