@@ -80,19 +80,19 @@ cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int6
                             int64_t strideD, void* stream);
 
 /* Split-K GEMM: the strided-batched GEMM of cy_gemm_batched with the K dimension of
- * every output tile divided among `splits` work units, so that shapes with few output tiles and a
- * long K (wave-quantised: the paper's small-size overheads) occupy every SM.  Each
- * split accumulates its k-range in TMEM and writes an fp32 partial slice to `workspace`; the split
- * that finishes a tile last sums the tile's partials in split order (deterministic, independent of
- * arrival order; integer-valued inputs stay exact) and runs the usual epilogue (alpha, beta*C,
- * one RN cast).  splits = 0: the library's cost model picks the count (1 = no split, the
- * cy_gemm_batched kernel); splits = S >= 1: S (reduced to the largest count that leaves no split
- * empty).  workspace: device memory of at least cy_gemm_splitk_workspace_size() bytes for the same
- * arguments, 16-byte aligned, any contents (the arrival counters carry a per-launch tag, so stale
- * bytes never count); it may be reused by later calls on the same stream, with any shape, but not by
- * concurrent calls.  It must not overlap A, B, C or D.  Errors as cy_gemm_batched, plus CY_ERR_INVALID_VALUE for splits
- * outside 0..64 or a workspace smaller than a requested split needs, CY_ERR_MISALIGNED for a
- * misaligned workspace. */
+ * every output tile divided among `splits` CTAs (or CTA pairs) that form one thread-block cluster,
+ * so that shapes with few output tiles and a long K (wave-quantised: the paper's small-size
+ * overheads) occupy every SM.  Each split accumulates its k-range in TMEM and writes an
+ * fp32 partial slice to `workspace`; after a cluster barrier every split reduces a share of the
+ * tile's chunks over all splits, in split order (deterministic, independent of timing;
+ * integer-valued inputs stay exact), and runs the usual epilogue on them (alpha, beta*C, one RN
+ * cast).  splits = 0: the library's cost model picks the count (1 = no split, the cy_gemm_batched
+ * kernel); splits = S >= 1: S, capped at 8 CTAs per cluster and reduced to the largest count that
+ * leaves no split empty.  workspace: device memory of at least cy_gemm_splitk_workspace_size()
+ * bytes for the same arguments, 16-byte aligned, any contents; it may be reused by later calls on
+ * the same stream, with any shape, but not by concurrent calls.  It must not overlap A, B, C or D.
+ * Errors as cy_gemm_batched, plus CY_ERR_INVALID_VALUE for splits outside 0..64 or a workspace
+ * smaller than a requested split needs, CY_ERR_MISALIGNED for a misaligned workspace. */
 cy_status_t cy_gemm_splitk(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, float alpha,
                            const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
                            int64_t strideB, float beta, const void* C, int64_t ldc, int64_t strideC, void* D,

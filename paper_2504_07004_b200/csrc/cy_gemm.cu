@@ -119,7 +119,7 @@ struct DevState {
   bool ok = false;
   int sms = 0;
   std::vector<char> attr_set;  // per menu entry: max dynamic smem attribute applied
-  std::vector<int> max_clusters;  // per menu entry: co-resident clusters (0 = not queried yet)
+  std::vector<int> max_clusters;  // per (menu entry, cluster size 1..8): co-resident clusters (0 = not queried)
 };
 std::mutex g_mu;
 DevState g_dev[64];
@@ -137,7 +137,7 @@ cy_status_t device_state(int& dev, DevState*& st) {
     cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev);
     st->ok = (major == 10 && minor == 0);
     st->attr_set.assign(menu().size(), 0);
-    st->max_clusters.assign(menu().size(), 0);
+    st->max_clusters.assign(menu().size() * 9, 0);
     if (!g_encode) {
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q;
@@ -234,11 +234,60 @@ bool overlap(Range a, Range b) { return a.lo < a.hi && b.lo < b.hi && a.lo < b.h
 
 // ------------------------------------------------------------------------------------------
 // config choice: minimise (waves x tile area / efficiency)
-double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k, int64_t L, int sms, int splits = 1) {
-  // time ~ waves x (tile area per SM) x (K + exposed epilogue) / efficiency
+// Kernel attributes (dynamic shared memory) of menu entry `idx`, set once per device.
+bool ensure_attr(DevState* st, int idx) {
+  const KDesc& kd = menu()[idx];
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!st->attr_set[idx]) {
+    if (cudaFuncSetAttribute(kd.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kd.smem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (kd.cg == 2) cudaFuncSetAttribute(kd.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    st->attr_set[idx] = 1;
+  }
+  return true;
+}
+
+// Co-resident clusters of `csize` CTAs of menu entry `idx` (clusters of 4 or 8 do not tile every
+// GPC: ask the occupancy calculator once and cache it).
+int active_clusters(DevState* st, int idx, int csize) {
+  if (csize <= 2) return std::max(1, st->sms / csize);
+  int& maxc = st->max_clusters[idx * 9 + csize];
+  if (maxc > 0) return maxc;
+  const KDesc& kd = menu()[idx];
+  int nc = 0;
+  if (ensure_attr(st, idx)) {
+    cudaLaunchConfig_t q;
+    std::memset(&q, 0, sizeof(q));
+    q.gridDim = dim3(csize * 256, 1, 1);
+    q.blockDim = dim3(kd.threads, 1, 1);
+    q.dynamicSmemBytes = kd.smem;
+    cudaLaunchAttribute qa;
+    qa.id = cudaLaunchAttributeClusterDimension;
+    qa.val.clusterDim.x = csize;
+    qa.val.clusterDim.y = 1;
+    qa.val.clusterDim.z = 1;
+    q.attrs = &qa;
+    q.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&nc, kd.fn, &q) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = st->sms / csize;
+    }
+  } else {
+    nc = st->sms / csize;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  maxc = nc;
+  return nc;
+}
+
+// Predicted time of one launch: waves x (tile area per SM) x (K + exposed epilogue) / efficiency.
+// `units` = tiles in flight (co-resident clusters; a split-K cluster works on one tile).
+double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k, int64_t L, int64_t units,
+                int splits = 1) {
   const int64_t bm = 128 * cg;
-  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn) * splits;
-  const int64_t units = sms / cg;
+  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
   const int64_t waves = (tiles + units - 1) / units;
   // relative per-SM efficiency of each tile shape, measured on B200 at 8192^3 under the power cap
   // (shared-memory operand bytes per MMA and L2 bytes per FLOP fall as the tile grows)
@@ -251,10 +300,10 @@ double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k,
   const int64_t kb = (k + 63) / 64;
   const int64_t kb_split = (kb + splits - 1) / splits;
   double kk = static_cast<double>(std::max<int64_t>(kb_split * 64, 64)) + (single_buf ? 128.0 : 0.0) + 128.0;
-  // split-K: every split writes its 128 x bn fp32 partial per CTA (~8 bn cycles at ~64 B/clk of
-  // L2 bandwidth) and the last one reads all `splits` partials back; one k-block costs 2 bn cycles
-  // per SM, so the reduction weighs (splits + 1) * 4 k-blocks = (splits + 1) * 256 K elements
-  if (splits > 1) kk += (splits + 1) * 256.0;
+  // split-K: every CTA writes its 128 x bn fp32 partial (~8 bn cycles at ~64 B/clk of L2
+  // bandwidth) and reads back the same volume for its share of the reduction; one k-block costs
+  // 2 bn cycles per SM, so the reduction weighs ~8 k-blocks = 512 K elements
+  if (splits > 1) kk += 512.0;
   return static_cast<double>(waves) * static_cast<double>(bm * bn) / cg * kk / eff;
 }
 
@@ -265,7 +314,7 @@ struct Choice {
 };
 size_t splitk_ws_bytes(const KDesc& kd, int64_t m, int64_t n, int64_t L, int splits);
 
-Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms, int max_splits = 1,
+Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, DevState* st, int max_splits = 1,
             size_t ws_bytes = 0, int forced_splits = 0, bool use_forced = true) {
   const auto& mn = menu();
   Choice best;
@@ -290,12 +339,16 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms
     const int single = acc_cols * 2 > 512;
     const bool can_split = var == cy::V_GEMM && mn[i].mc == 1 && mn[i].bn <= 256;  // one accumulator (NSUB 1)
     if (!can_split && forced_splits > 1) continue;  // a requested split needs a splittable kernel
-    const int s_hi = can_split ? static_cast<int>(std::min<int64_t>(max_splits, std::max<int64_t>(kb, 1))) : 1;
+    // split-K clusters: cta_group x splits <= 8 CTAs (portable cluster size)
+    const int s_cap = 8 / mn[i].cg;
+    const int s_hi = can_split ? static_cast<int>(std::min<int64_t>(std::min(max_splits, s_cap), std::max<int64_t>(kb, 1)))
+                               : 1;
     for (int sp = 1; sp <= s_hi; ++sp) {
       if (eff_splits(sp) != sp) continue;  // same k-block ranges as a smaller count
       if (can_split && forced_splits > 0 && sp != eff_splits(std::min(forced_splits, s_hi))) continue;
       if (sp > 1 && splitk_ws_bytes(mn[i], m, n, L, sp) > ws_bytes) continue;
-      const double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, sms, sp);
+      const int cl = mn[i].cg * mn[i].mc * sp;
+      const double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, active_clusters(st, static_cast<int>(i), cl), sp);
       if (best.idx < 0 || c < best_cost) {
         best.idx = static_cast<int>(i);
         best.splits = sp;
@@ -304,24 +357,16 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, int sms
     }
   }
   if (best.idx < 0 && forced >= 0)  // the forced shape has no kernel of this variant: heuristic
-    return pick(var, dt, m, n, k, L, sms, max_splits, ws_bytes, forced_splits, false);
+    return pick(var, dt, m, n, k, L, st, max_splits, ws_bytes, forced_splits, false);
   return best;
 }
 
-// Split-K workspace: [counters: one 64-bit epoch-tagged count per (tile, CTA, epilogue warp), padded
-// to 256 B]
-// [partials: tiles x CTAs x 128 rows x TILE_N fp32 per split].
-size_t splitk_counter_bytes(const KDesc& kd, int64_t m, int64_t n, int64_t L) {
-  const int64_t bm = 128 * kd.cg * kd.mc;
-  const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + kd.bn - 1) / kd.bn);
-  const int epi_warps = kd.threads / 32 - 2;  // V_GEMM: producer + MMA + epilogue warps
-  return static_cast<size_t>((tiles * kd.cg * epi_warps * 8 + 255) / 256 * 256);
-}
+// Split-K workspace: the fp32 partial slices, tiles x CTAs per tile x 128 rows x TILE_N x splits.
 size_t splitk_ws_bytes(const KDesc& kd, int64_t m, int64_t n, int64_t L, int splits) {
   if (splits <= 1) return 0;
   const int64_t bm = 128 * kd.cg * kd.mc;
   const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + kd.bn - 1) / kd.bn);
-  return splitk_counter_bytes(kd, m, n, L) + static_cast<size_t>(tiles * kd.cg * 128 * kd.bn * 4) * splits;
+  return static_cast<size_t>(tiles * kd.cg * 128 * kd.bn * 4) * splits;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -339,7 +384,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   cy_status_t s = device_state(dev, st);
   if (s != CY_OK) return s;
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX || L > INT32_MAX) return CY_ERR_INVALID_VALUE;
-  const Choice ch = pick(var, dt, m, n, k, L, st->sms, max_splits, ws_bytes, forced_splits);
+  const Choice ch = pick(var, dt, m, n, k, L, st, max_splits, ws_bytes, forced_splits);
   const int idx = ch.idx;
   if (idx < 0) return CY_ERR_INTERNAL;
   const KDesc& kd = menu()[idx];
@@ -381,19 +426,9 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.k_blocks = (int)((k + 63) / 64);
   p.splits = ch.splits;
   p.kb_split = p.splits > 1 ? (p.k_blocks + p.splits - 1) / p.splits : p.k_blocks;
-  p.ws = nullptr;
-  p.ws_cnt = nullptr;
-  p.epoch = 0;
-  if (p.splits > 1) {
-    static std::atomic<unsigned int> g_epoch{0};
-    unsigned int e = g_epoch.fetch_add(1) + 1;
-    if (e == 0) e = g_epoch.fetch_add(1) + 1;  // 0 is never a launch tag
-    p.epoch = e;
-    p.ws_cnt = static_cast<unsigned long long*>(ws);
-    p.ws = reinterpret_cast<float*>(static_cast<char*>(ws) + splitk_counter_bytes(kd, m, n, L));
-  }
-  if (L * p.m_blocks * p.n_blocks * p.splits > INT32_MAX) return CY_ERR_INVALID_VALUE;
-  p.tiles = (int)(L * p.m_blocks * p.n_blocks * p.splits);
+  p.ws = p.splits > 1 ? static_cast<float*>(ws) : nullptr;
+  if (L * p.m_blocks * p.n_blocks > INT32_MAX) return CY_ERR_INVALID_VALUE;
+  p.tiles = (int)(L * p.m_blocks * p.n_blocks);
   p.group_m = g_group_m > 0 ? g_group_m : 12;  // measured 8192^3 / 65536x8192^2: 6 8 12 16 24 -> 12 best (profiles/r02_group_m.md)
   p.l2_policy = g_l2_policy;
   p.sleep_ns = g_sleep_ns;
@@ -402,40 +437,10 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.n_extra = n_extra;
   p.y = y;
 
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!st->attr_set[idx]) {
-      if (cudaFuncSetAttribute(kd.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kd.smem) != cudaSuccess) {
-        cudaGetLastError();
-        return CY_ERR_LAUNCH;
-      }
-      if (kd.cg == 2) cudaFuncSetAttribute(kd.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-      st->attr_set[idx] = 1;
-    }
-  }
-  const int csize = kd.cg * kd.mc;
-  if (kd.mc > 1 && st->max_clusters[idx] == 0) {  // clusters of 4 do not tile every GPC: ask
-    cudaLaunchConfig_t q;
-    std::memset(&q, 0, sizeof(q));
-    q.gridDim = dim3(csize * 256, 1, 1);
-    q.blockDim = dim3(kd.threads, 1, 1);
-    q.dynamicSmemBytes = kd.smem;
-    cudaLaunchAttribute qa;
-    qa.id = cudaLaunchAttributeClusterDimension;
-    qa.val.clusterDim.x = csize;
-    qa.val.clusterDim.y = 1;
-    qa.val.clusterDim.z = 1;
-    q.attrs = &qa;
-    q.numAttrs = 1;
-    int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, kd.fn, &q) != cudaSuccess || nc <= 0) {
-      cudaGetLastError();
-      nc = st->sms / csize;
-    }
-    std::lock_guard<std::mutex> lk(g_mu);
-    st->max_clusters[idx] = nc;
-  }
-  const int units = kd.mc > 1 ? st->max_clusters[idx] : std::max(1, st->sms / kd.cg);
+  if (!ensure_attr(st, idx)) return CY_ERR_LAUNCH;
+  const int csize = kd.cg * kd.mc * p.splits;  // split-K: the splits of a tile form one cluster
+  if (csize > 8) return CY_ERR_INTERNAL;
+  const int units = active_clusters(st, idx, csize);
   // More tiles than co-resident clusters: launch one cluster per tile and let running clusters
   // steal pending ones (cluster launch control) so the tiles in flight stay adjacent in the
   // raster; otherwise every tile gets its own resident cluster.
@@ -631,8 +636,8 @@ cy_status_t cy_gemm_batched(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int6
 
 // split-K: the choice the library makes for (shape, splits) with an unbounded workspace
 static constexpr int kMaxAutoSplits = 16;
-static Choice splitk_choice(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, int splits, int sms) {
-  return pick(cy::V_GEMM, dt, m, n, k, batch, sms, splits == 0 ? kMaxAutoSplits : splits, SIZE_MAX, splits);
+static Choice splitk_choice(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, int splits, DevState* st) {
+  return pick(cy::V_GEMM, dt, m, n, k, batch, st, splits == 0 ? kMaxAutoSplits : splits, SIZE_MAX, splits);
 }
 
 size_t cy_gemm_splitk_workspace_size(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64_t batch, int splits) {
@@ -641,7 +646,7 @@ size_t cy_gemm_splitk_workspace_size(cy_dtype_t dt, int64_t m, int64_t n, int64_
   int dev;
   DevState* st;
   if (device_state(dev, st) != CY_OK) return 0;
-  const Choice ch = splitk_choice(dt, m, n, k, batch, splits, st->sms);
+  const Choice ch = splitk_choice(dt, m, n, k, batch, splits, st);
   if (ch.idx < 0) return 0;
   return splitk_ws_bytes(menu()[ch.idx], m, n, batch, ch.splits);
 }
@@ -669,7 +674,7 @@ cy_status_t cy_gemm_splitk(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, int64
     DevState* st;
     s = device_state(dev, st);
     if (s != CY_OK) return s;
-    const Choice ch = splitk_choice(dt, m, n, k, batch, splits, st->sms);
+    const Choice ch = splitk_choice(dt, m, n, k, batch, splits, st);
     if (ch.idx >= 0 && splitk_ws_bytes(menu()[ch.idx], m, n, batch, ch.splits) > workspace_bytes)
       return CY_ERR_INVALID_VALUE;
   }

@@ -50,7 +50,7 @@ struct Params {
   float alpha, beta;
   int has_c;             // beta != 0: C is read
   int m_blocks, n_blocks, k_blocks;
-  int tiles;             // work units: L * m_blocks * n_blocks * splits
+  int tiles;             // L * m_blocks * n_blocks
   int group_m;           // grouped rasterisation width (in m-blocks)
   int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
   float* y;              // V_ROWREDUCE: y[M]
@@ -58,11 +58,10 @@ struct Params {
   int n_extra;           // number of extra D destinations in DstMaps (0 = D only)
   int a_reuse;           // 1: two-slot k-blocks interleave MMAs with the A collector buffer
   int sleep_ns;          // >0: epilogue waits for the accumulator with nanosleep backoff (cap, ns)
-  int splits;            // split-K (V_GEMM): work unit u = tile u / splits, k-blocks of split u % splits
+  int splits;            // split-K (V_GEMM, one accumulator): CTA (pair) s of a cluster of `splits`
+                         // CTAs (pairs) takes k-blocks [s*kb_split, (s+1)*kb_split) of the cluster's tile
   int kb_split;          // k-blocks per split (the last split may hold fewer; every split holds >= 1)
   float* ws;             // split-K: fp32 partial slices (cy_gemm_splitk workspace)
-  unsigned long long* ws_cnt;  // split-K: per-slice arrival counters, (launch epoch << 32) | arrivals
-  unsigned int epoch;    // split-K: this launch's tag (non-zero, different from the previous launches')
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride;
                          // 2: one cluster per tile, no stealing (non-persistent)
@@ -121,6 +120,9 @@ struct Cfg {
   static constexpr int SCHED_SLOTS = 4;       // tile-ID ring depth (dynamic schedule)
   static constexpr int NUM_WARPS = THREADS / 32;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  // split-K across the CTAs (pairs) of a cluster: plain GEMM tiles with one accumulator
+  static constexpr bool SPLITTABLE = (VAR == V_GEMM && MC == 1 && NSUB == 1);
+  static_assert(24 * STAGES + 232 + 8 * EPI_WARPS <= BAR_BYTES, "barrier region");
   // Row-reduce: the reducer warps learn that their CTA's A stage is in shared memory from a
   // second tcgen05.commit (bMDone, multicast to both CTAs of a pair) issued after the MMAs that
   // read the stage; the stage is released only when the MMAs and the reducers are both done.
@@ -156,11 +158,11 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& b, int&
   nb = rg / gm;
 }
 
-// Work unit u (split-K: tile u / splits, k-block range of split u % splits).
-__device__ __forceinline__ void unit_coords(const Params& p, int u, int& b, int& mb, int& nb, int& kb0, int& kb1) {
-  const int tile = u / p.splits;
-  tile_coords(p, tile, b, mb, nb);
-  kb0 = (u - tile * p.splits) * p.kb_split;
+// Tile t and the k-block range [kb0, kb1) of split `sidx` (0 when not split).
+__device__ __forceinline__ void unit_coords(const Params& p, int t, int sidx, int& b, int& mb, int& nb, int& kb0,
+                                            int& kb1) {
+  tile_coords(p, t, b, mb, nb);
+  kb0 = sidx * p.kb_split;
   kb1 = min(p.k_blocks, kb0 + p.kb_split);
 }
 
@@ -216,16 +218,21 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const uint32_t bSFull = bTFull + 104;                      // [SCHED_SLOTS] tile-ID ring: response landed
   const uint32_t bSEmpty = bSFull + 8 * C::SCHED_SLOTS;      // [SCHED_SLOTS] all warps of the cluster read it
   const uint32_t sResp = (bSEmpty + 8 * C::SCHED_SLOTS + 15u) & ~15u;  // [SCHED_SLOTS] x 16-B responses
+  const uint32_t bRed = sResp + 16 * C::SCHED_SLOTS;         // [EPI_WARPS] split-K: partials of every split written
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t crank = (C::CL > 1) ? cluster_ctarank() : 0u;  // rank in the cluster
+  // split-K: the cluster is `splits` CTAs (pairs) stacked along K, all on the same output tile
+  const int SPL = C::SPLITTABLE ? p.splits : 1;
+  const int CLr = C::CL * SPL;                                  // cluster size (run time)
+  const uint32_t crank = (CLr > 1) ? cluster_ctarank() : 0u;    // rank in the cluster
   const uint32_t rank = crank & (C::CG - 1);                    // rank in the CTA pair
-  const uint32_t pp = crank / C::CG;                            // pair index in the cluster (MC == 2)
+  const uint32_t pp = (C::MC == 2) ? crank / C::CG : 0u;        // pair index in the cluster (MC == 2)
+  const int sidx = (SPL > 1) ? int(crank / C::CG) : 0;          // split index (split-K)
   const uint32_t leader = crank & ~uint32_t(C::CG - 1);         // this pair's MMA leader
-  const int cid = blockIdx.x / C::CL;
-  const int ncl = gridDim.x / C::CL;
+  const int cid = blockIdx.x / CLr;
+  const int ncl = gridDim.x / CLr;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -247,8 +254,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(bCBar + 8 * w, 1);
     for (int j = 0; j < C::SCHED_SLOTS; ++j) {
       mbar_init(bSFull + 8 * j, 1);
-      mbar_init(bSEmpty + 8 * j, C::CL * C::NUM_WARPS);
+      mbar_init(bSEmpty + 8 * j, CLr * C::NUM_WARPS);
     }
+    if (SPL > 1)
+      for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(bRed + 8 * w, SPL);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     tmem_relinquish<C::CG>();
   }
   tc_fence_before();
-  if constexpr (C::CL > 1) cluster_sync(); else __syncthreads();
+  if (CLr > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Everything above (barrier init, TMEM allocation, descriptor prefetch) overlapped the tail of
@@ -285,10 +294,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     clc_decode(sResp + 16 * j, ok, cx);
     if (warp_wide) __syncwarp();
     if (!warp_wide || lane == 0) {
-      if constexpr (C::CL > 1) mbar_arrive_cluster(mapa(bSEmpty + 8 * j, 0));
+      if (CLr > 1) mbar_arrive_cluster(mapa(bSEmpty + 8 * j, 0));
       else mbar_arrive(bSEmpty + 8 * j);
     }
-    t = static_cast<int>(cx) / C::CL;
+    t = static_cast<int>(cx) / CLr;
     return ok != 0;
   };
   // Producer thread, at the start of its tile i: arm this CTA's slot for tile i+1 and (leader)
@@ -299,7 +308,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     mbar_arrive_expect_tx(bSFull + 8 * j, 16);
     if (crank == 0) {
       mbar_wait(bSEmpty + 8 * j, ((i / C::SCHED_SLOTS) & 1) ^ 1);
-      if constexpr (C::CL > 1) clc_try_cancel_multicast(sResp + 16 * j, bSFull + 8 * j);
+      if (CLr > 1) clc_try_cancel_multicast(sResp + 16 * j, bSFull + 8 * j);
       else clc_try_cancel(sResp + 16 * j, bSFull + 8 * j);
     }
   };
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       for (int i = 0; sched_next(i, t, false); ++i) {
         sched_request(i);
         int b, mb, nb, kb0, kb1;
-        unit_coords(p, t, b, mb, nb, kb0, kb1);
+        unit_coords(p, t, sidx, b, mb, nb, kb0, kb1);
         const int am = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA;
         const int bn = nb * C::TILE_N + rank * C::BN_CTA;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -417,7 +426,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       };
       auto release = [&](int st) {
-        mma_commit<C::CG>(bEmpty + 8 * st, kAllMask);  // frees the stage (B multicast: in both pairs)
+        // frees the stage: in both CTAs of the pair (B multicast, MC == 2: in both pairs)
+        mma_commit<C::CG>(bEmpty + 8 * st, C::MC == 2 ? kAllMask : pair_mask);
         if constexpr (C::REDUCE) mma_commit<C::CG>(bMDone + 8 * st, pair_mask);  // reducers may read it
       };
       int t;
@@ -426,7 +436,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
         const uint32_t d = tmem_base + buf * C::ACC_COLS;
         int ub, umb, unb, kb0, kb1;
-        unit_coords(p, t, ub, umb, unb, kb0, kb1);
+        unit_coords(p, t, sidx, ub, umb, unb, kb0, kb1);
         kfirst = kb0;
         if constexpr (!C::SPLIT) {
           mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
@@ -531,11 +541,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     };
     int t;
-    // C prefetch: not with split-K (only the last-arriving split of a tile stores it)
-    const bool cpf = CPF && p.has_c && p.splits == 1;
+    // C prefetch: not with split-K (each split stores only some of its chunks)
+    const bool cpf = CPF && p.has_c && SPL == 1;
+    uint32_t red_phase = 0;  // split-K: parity of this warp's bRed barrier
     for (int it = 0; sched_next(it, t, true); ++it) {
       int b, mb, nb, kb0, kb1;
-      unit_coords(p, t, b, mb, nb, kb0, kb1);
+      unit_coords(p, t, sidx, b, mb, nb, kb0, kb1);
       const bool has_k = kb1 > kb0;
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
@@ -652,23 +663,24 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       };
       if constexpr (C::VAR == V_GEMM && C::MC == 1 && C::NSUB == 1) {  // (the host splits only these)
-        if (p.splits > 1) {
-          // ---- split-K: every split of a tile writes its fp32 partial slice
-          // (this warp's 32 rows x NQ chunks) to the workspace and counts itself in; the split that
-          // arrives last sums all slices in split order (deterministic, independent of arrival
-          // order) and runs the normal epilogue.  Slice layout: float4 j of lane l of chunk q at
-          // ((q*16 + j)*32 + l): every warp-wide access is 512 contiguous bytes.
-          const int tile = t / p.splits, sp = t - tile * p.splits;
-          const int wslot = (tile * C::CG + int(rank)) * C::EPI_WARPS + ew;
+        if (SPL > 1) {
+          // ---- split-K: the cluster's SPL CTAs (pairs) each hold the partial sum of
+          // their k-range.  Every epilogue warp writes its slice (32 rows x NQ chunks, fp32) to the
+          // workspace and arrives on the same warp's barrier in every split CTA of its pair half;
+          // then warp `ew` of split s reduces the chunks q = s (mod SPL) over all splits, in split
+          // order (deterministic), and stores them.  The splits share the reduction; the cluster
+          // guarantees they are co-resident.  Slice layout: float4 j of lane l of chunk q at
+          // ((q*16 + j)*32 + l) -- every warp-wide access is 512 contiguous bytes.
+          const int wslot = (t * C::CG + int(rank)) * C::EPI_WARPS + ew;
           constexpr int SLICE4 = NQ * 16 * 32;  // float4 per slice
-          float4* wsl = reinterpret_cast<float4*>(p.ws) + size_t(wslot) * p.splits * SLICE4;
+          float4* wsl = reinterpret_cast<float4*>(p.ws) + size_t(wslot) * SPL * SLICE4;
           uint32_t gt[C::GLU ? 64 : 1];
 #pragma unroll 1
           for (int q = 0; q < NQ; ++q) {
             uint32_t r[64];
             load_chunk(q, r, gt);
             if ((q + 1) % CPW == 0) release(q / CPW);
-            float4* dst = wsl + size_t(sp) * SLICE4 + q * 16 * 32 + lane;
+            float4* dst = wsl + size_t(sidx) * SLICE4 + q * 16 * 32 + lane;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               __stcg(dst + 32 * j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
@@ -676,28 +688,15 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           }
           __threadfence();
           __syncwarp();
-          // arrivals before ours in this launch: a counter tagged with another launch's epoch (left by
-          // an earlier call, or workspace bytes an earlier call used otherwise) counts as zero, so the
-          // workspace needs no zero fill and no reset
-          int before = 0;
-          if (lane == 0) {
-            unsigned long long* cnt = p.ws_cnt + wslot;
-            unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(cnt), want;
-            do {
-              want = seen;
-              const bool mine = static_cast<unsigned int>(want >> 32) == p.epoch;
-              before = mine ? static_cast<int>(want & 0xffffffffull) : 0;
-              seen = atomicCAS(cnt, want, mine ? want + 1 : ((static_cast<unsigned long long>(p.epoch) << 32) | 1ull));
-            } while (seen != want);
-          }
-          before = __shfl_sync(0xffffffffu, before, 0);
-          if (before != p.splits - 1) continue;  // another split of this tile finishes it
-          __threadfence();
+          if (lane < SPL)  // lane s: our slice is written -> split s's barrier for this warp
+            mbar_arrive_release_cluster(mapa(bRed + 8 * ew, uint32_t(lane * C::CG) + rank));
+          mbar_wait_acquire_cluster(bRed + 8 * ew, red_phase);
+          red_phase ^= 1;
 #pragma unroll 1
-          for (int q = 0; q < NQ; ++q) {
+          for (int q = sidx; q < NQ; q += SPL) {
             uint32_t r[64];
 #pragma unroll 1
-            for (int s2 = 0; s2 < p.splits; ++s2) {
+            for (int s2 = 0; s2 < SPL; ++s2) {
               const float4* src = wsl + size_t(s2) * SLICE4 + q * 16 * 32 + lane;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -811,7 +810,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 
   __syncwarp();
   tc_fence_before();
-  if constexpr (C::CL > 1) cluster_sync(); else __syncthreads();
+  if (CLr > 1) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::CG>(tmem_base, C::TMEM_COLS);
