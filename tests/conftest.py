@@ -9,6 +9,12 @@ if ROOT not in sys.path:
 
 
 def pytest_configure(config):
+    # timing/variant experiments only: run the tests against an experiment build of the library
+    exp = os.environ.get("CY_ATTN_EXPERIMENTS_LIB")
+    if exp:
+        from paper_2504_07004_b200 import _lib
+
+        _lib.use_library(os.path.abspath(exp))
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
