@@ -657,9 +657,13 @@ def main():
     value = W["flops"] * world / (ms_per_step * 1e-3) / 1e12
     peaks = load_peaks()
     achieved = W["kernel_flops"] / (kern_ms * 1e-3) / 1e12
-    # The roofline denominator follows what the clocks saw during the timed region: the sustained
-    # (power-capped) cuBLAS figure when sw_power_cap was active, the burst figure otherwise.
-    power_capped = "sw_power_cap" in sampler.reasons
+    # The roofline denominator follows what the clocks did during the timed region: the sustained
+    # (power-capped) cuBLAS figure when sw_power_cap was active AND pulled the median SM clock below
+    # 90 % of its maximum (the sustained figure was measured at ~1.35 GHz), the burst figure
+    # otherwise (a short region can see the cap flag while still running near full clock).
+    cs = sampler.summary()
+    power_capped = ("sw_power_cap" in sampler.reasons and cs.get("sm_mhz") is not None
+                    and cs.get("sm_max_mhz") and cs["sm_mhz"] < 0.9 * cs["sm_max_mhz"])
     peak = peaks["sustained"] if power_capped else peaks["burst"]
 
     e2e = None
@@ -699,8 +703,8 @@ def main():
             "pct_of_nominal_2250": round(100.0 * value / world / 2250.0, 2),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": load_traffic(args.workload),
-                         "peak_source": peaks["source"] + ("; sustained figure (sw_power_cap active during the timed region)"
-                                                           if power_capped else "; burst figure (no power-cap reason during the timed region)"),
+                         "peak_source": peaks["source"] + ("; sustained figure (sw_power_cap active, median SM clock < 90 % of max during the timed region)"
+                                                           if power_capped else "; burst figure (SM clock near max during the timed region)"),
                          "frac_of_burst": round(achieved / peaks["burst"], 4),
                          "frac_of_sustained": round(achieved / peaks["sustained"], 4),
                          "kernel_ms": round(kern_ms, 5)},

@@ -88,7 +88,7 @@ constexpr int SK_OFF = NT * TILE;          // [2]
 constexpr int SV_OFF = (NT + 2) * TILE;    // [2]
 constexpr int BAR_OFF = (NT + 4) * TILE;
 constexpr int XCH_OFF = BAR_OFF + 256;       // CS = 2: row-max exchange [NT][2][2][BQ], sums [NT][2][BQ]
-constexpr int SMEM_BYTES = 1024 + (NT + 4) * TILE + 256 + (NT * 2 * 2 * BQ + NT * 2 * BQ) * 4;
+[[maybe_unused]] constexpr int SMEM_BYTES = 1024 + (NT + 4) * TILE + 256 + (NT * 2 * 2 * BQ + NT * 2 * BQ) * 4;
 // CS = 3 layout: V gets a third ring slot (a K/V tile load takes ~4-5 K cycles under load, longer than
 // the lead two slots give); barriers after the last V slot, no exchange area
 #ifndef CY_ATTN_VS3
@@ -809,6 +809,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
 
 
 
+#ifdef CY_ATTN_EXPERIMENTS  // measured slower than the default: experiment build only
 // ============================================================================ persistent two-tile kernel
 // The default layout (two 128-row query tiles per CTA, softmax warpgroup per tile, setmaxnreg)
 // made persistent: one CTA per SM walks the work items (query-tile pair, batch*head) -- the
@@ -1481,6 +1482,8 @@ __global__ void __launch_bounds__(pr::threads<NS>(), 1)
   }
 }
 
+#endif  // CY_ATTN_EXPERIMENTS
+
 // ------------------------------------------------------------------------------------------ host
 std::once_flag g_once;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1637,11 +1640,14 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
 #else
   p.l2hint = 1;  // evict_last on Q/K/V (measured: without it causal 16384 loses 6 %)
   constexpr int ki = 4, ei = 0;
-  constexpr bool ps = false;
   const int cs = 3;
   const void* fn = dt == CY_F16 ? (const void*)&attn_fwd_kernel<0, 0, 3> : (const void*)&attn_fwd_kernel<1, 0, 3>;
 #endif
+#ifdef CY_ATTN_EXPERIMENTS
   const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : (kern == 1 && cs == 3) ? SMEM_BYTES3 : SMEM_BYTES;
+#else
+  const int smem = SMEM_BYTES3;
+#endif
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     if (!g_attr_set[dev][ki][dt][ei]) {
@@ -1658,6 +1664,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
+#ifdef CY_ATTN_EXPERIMENTS
   if (kern == 2) {
     cfg.gridDim = dim3((unsigned)(2 * ((seq_q + 2 * BQ - 1) / (2 * BQ))), (unsigned)bh, 1);
     cfg.blockDim = dim3(split == 2 ? pr::threads<2>() : pr::threads<4>(), 1, 1);
@@ -1671,7 +1678,9 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
     cfg.gridDim = dim3((unsigned)std::min<int64_t>(items, std::max(1, g_sms[dev])), 1, 1);
     cfg.blockDim = dim3(384, 1, 1);
     cfg.numAttrs = 1;
-  } else {
+  } else
+#endif
+  {
     cfg.gridDim = dim3((unsigned)((seq_q + BQ * NT - 1) / (BQ * NT)), (unsigned)bh, 1);
     cfg.blockDim = dim3(cs == 3 ? 384 : THREADS, 1, 1);
     cfg.numAttrs = 1;
