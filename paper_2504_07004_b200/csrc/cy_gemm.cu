@@ -521,6 +521,18 @@ cy_status_t launch_rowsum(int dt, const void* A, int64_t lda, int64_t m, int64_t
 
 }  // namespace
 
+#ifdef CY_GEMM_TRACE
+// trace build only (scripts/build_experiment.py gtrace CY_GEMM_TRACE=1): not in the product ABI
+extern "C" int cy_gemm_trace_read(unsigned long long* out, int clear) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(g_gemm_trace));
+  if (clear) {
+    static unsigned long long zero[64 * 16] = {};
+    cudaMemcpyToSymbol(g_gemm_trace, zero, sizeof(zero));
+  }
+  return static_cast<int>(e);
+}
+#endif
+
 // shared with the attention entry point (cy_attention.cu): every kernel this library launches
 namespace cy_internal {
 void note_launch() { g_launches.fetch_add(1); }

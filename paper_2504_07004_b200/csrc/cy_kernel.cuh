@@ -39,6 +39,30 @@
 #define CY_DEBUG_MODE 0
 #endif
 
+// CY_GEMM_TRACE (timing experiments only, never in the product build): clock64() stamps of one
+// CTA's per-tile events (scripts/gemm_trace.py reads them with cy_gemm_trace_read()).
+#ifdef CY_GEMM_TRACE
+#ifndef CY_GEMM_TRACE_CTA
+#define CY_GEMM_TRACE_CTA 0
+#endif
+__device__ unsigned long long g_gemm_trace[64 * 16];
+#define CY_TR(it, ev)                                                                      \
+  do {                                                                                     \
+    if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) < 64) g_gemm_trace[(it) * 16 + (ev)] = clock64(); \
+  } while (0)
+#define CY_TR_ADD(it, ev, v)                                                               \
+  do {                                                                                     \
+    if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) < 64) g_gemm_trace[(it) * 16 + (ev)] += (v);      \
+  } while (0)
+#else
+#define CY_TR(it, ev) \
+  do {                \
+  } while (0)
+#define CY_TR_ADD(it, ev, v) \
+  do {                       \
+  } while (0)
+#endif
+
 namespace cy {
 
 constexpr int kDebug = CY_DEBUG_MODE;
@@ -329,6 +353,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       constexpr bool PAIR_TMA = (C::CG == 2);
       int t;
       for (int i = 0; sched_next(i, t, false); ++i) {
+        CY_TR(i, 0);
         sched_request(i);
         int b, mb, nb, kb0, kb1;
         unit_coords(p, t, sidx, b, mb, nb, kb0, kb1);
@@ -336,6 +361,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const int bn = nb * C::TILE_N + rank * C::BN_CTA;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(bEmpty + 8 * stage, phase ^ 1);
+          if (kb == kb0) CY_TR(i, 1);
+          if (kb == kb1 - 1) CY_TR(i, 2);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
           if ((kDebug & 1) && (phase || i != 0)) {  // timing experiment: reuse stale stages
@@ -438,11 +465,23 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         int ub, umb, unb, kb0, kb1;
         unit_coords(p, t, sidx, ub, umb, unb, kb0, kb1);
         kfirst = kb0;
+        CY_TR(it, 3);
+#ifdef CY_GEMM_TRACE
+        auto wait_full = [&](int kb) {
+          const long long w0 = clock64();
+          mbar_wait(bFull + 8 * stage, phase);
+          CY_TR_ADD(it, 7, clock64() - w0);
+          if (kb == kb0) CY_TR(it, 5);
+        };
+#else
+        auto wait_full = [&](int) { mbar_wait(bFull + 8 * stage, phase); };
+#endif
         if constexpr (!C::SPLIT) {
           mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
+          CY_TR(it, 4);
           tc_fence_after();
           for (int kb = kb0; kb < kb1; ++kb) {
-            mbar_wait(bFull + 8 * stage, phase);
+            wait_full(kb);
             tc_fence_after();
             if constexpr (C::NUM_B == 2) {
               if (p.a_reuse) issue_both(d, stage, kb);
@@ -456,6 +495,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         } else {
           // bTEmpty[a] = accumulator a drained by both CTAs' epilogues
           mbar_wait(bTEmpty, bph ^ 1);
+          CY_TR(it, 4);
           tc_fence_after();
           bool acc1 = false;
           int held = 0, held0 = 0, held_kb0 = 0;
@@ -468,7 +508,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             held = 0;
           };
           for (int kb = kb0; kb < kb1; ++kb) {
-            mbar_wait(bFull + 8 * stage, phase);
+            wait_full(kb);
             tc_fence_after();
             if (acc1 && held == 0 && p.a_reuse) {  // steady state: both accumulators, A reused
               issue_both(d, stage, kb);
@@ -486,7 +526,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             if (acc1) {
               flush();
             } else if (held == C::STAGES) {  // every stage is held: wait for accumulator 1
+#ifdef CY_GEMM_TRACE
+              const long long w1 = clock64();
               mbar_wait(bTEmpty + 8, bph ^ 1);
+              CY_TR_ADD(it, 14, clock64() - w1);
+#else
+              mbar_wait(bTEmpty + 8, bph ^ 1);
+#endif
               acc1 = true;
               tc_fence_after();
               flush();
@@ -500,6 +546,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           }
         }
         mma_commit<C::CG>(bTFull + 8 * buf, pair_mask);  // accumulator ready, both CTAs of the pair
+        CY_TR(it, 6);
       }
     } else if (lane == 0) {
       // peer CTA: the leader issues all MMAs; follow the tile schedule only
@@ -552,8 +599,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
       const int row0 = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA + 32 * q4;
       if (cpf) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
+      if (ew == 0 && lane == 0) CY_TR(it, 8);
       if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
       else mbar_wait(bTFull + 8 * buf, bph);
+      if (ew == 0 && lane == 0) CY_TR(it, 9);
       tc_fence_after();
       if constexpr ((kDebug & 2) != 0) {  // timing experiment: drop the epilogue
         tc_fence_before();
@@ -579,11 +628,19 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             const uint32_t bar = bTEmpty + 8 * (C::SPLIT ? a : buf);
             if constexpr (C::CG == 2) mbar_arrive_cluster(mapa(bar, leader));
             else mbar_arrive(bar);
+            if (ew == 0) CY_TR(it, a == 0 ? 10 : 11);
           }
         }
       };
       // wait until the current slot may be written (no C) / holds chunk q's C tile
       auto slot_ready = [&](int q) {
+#ifdef CY_GEMM_TRACE
+        const long long w0 = clock64();
+        struct Add {
+          long long w0; int it, ew, lane;
+          __device__ ~Add() { if (ew == 0 && lane == 0) CY_TR_ADD(it, 13, clock64() - w0); }
+        } add{w0, it, ew, lane};
+#endif
         if (p.has_c) {
           if (!cpf) fetch_c(nb, row0, b, q, slot);
           mbar_wait(cbar, cphase);
@@ -602,6 +659,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           tma_store_3d(chunk_d(q), sb, n0, row0, b);
           for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
           bulk_commit();
+          if (ew == 0 && q == NQ - 1) CY_TR(it, 12);
         }
         if constexpr (C::EPI_BUFS == 2) slot ^= 1;
         if (cpf && q + 1 < NQ) fetch_c(nb, row0, b, q + 1, slot);  // next chunk's C
