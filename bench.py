@@ -259,7 +259,7 @@ def make_workload(name, rank, world, device):
             hy = torch.empty((m_rank,), dtype=torch.float32).pin_memory()
 
         def e2e_step(i):
-            j = i % nsets
+            j = i % len(hA)  # (the host keeps the first two input sets)
             if pipe is not None and name == "rowreduce":
                 pipe.submit((hA[j], hB[j]), (hD, hy))
                 return

@@ -75,19 +75,18 @@ const std::vector<KDesc>& menu() {
 }
 
 std::atomic<int> g_forced{-1};
-// CY_GROUP_M: rasterisation group width in m-blocks (tuning knob; default 8)
-const int g_group_m = [] {
-  const char* e = std::getenv("CY_GROUP_M");
-  return e ? std::atoi(e) : 0;
-}();
-// CY_L2_POLICY: TMA L2 eviction hints for A/B (tuning knob; see Params::l2_policy)
-// Default 5 = no cache hint: measured on B200 at 8192^3, hint-free TMA requests for the same lines
-// from different SMs are merged in L2 (22 % fewer L2 request sectors than with an evict_normal
-// policy), which under the power cap buys ~3 % clock.
-const int g_l2_policy = [] {
-  const char* e = std::getenv("CY_L2_POLICY");
-  return e ? std::atoi(e) : 5;
-}();
+// Tile order and L2 hints (tuning knobs; -1 = the defaults below, chosen per problem in launch()):
+// CY_RASTER 0 = groups of CY_GROUP_M m-blocks (A panels resident, B streams), 1 = groups of
+// CY_GROUP_M n-blocks (B panels resident, A streams); CY_SERP=1 reverses the sweep of odd groups;
+// CY_L2_POLICY = TMA L2 eviction hints for A/B (see Params::l2_policy).
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+const int g_group_m = env_int("CY_GROUP_M", 0);
+const int g_l2_policy = env_int("CY_L2_POLICY", -1);
+const int g_serp = env_int("CY_SERP", -1);
+const int g_raster = env_int("CY_RASTER", -1);
 // CY_SCHED: 0 = dynamic (cluster launch control) when there is more than one wave, 1 = static
 const int g_sched = [] {
   const char* e = std::getenv("CY_SCHED");
@@ -429,8 +428,16 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.ws = p.splits > 1 ? static_cast<float*>(ws) : nullptr;
   if (L * p.m_blocks * p.n_blocks > INT32_MAX) return CY_ERR_INVALID_VALUE;
   p.tiles = (int)(L * p.m_blocks * p.n_blocks);
-  p.group_m = g_group_m > 0 ? g_group_m : 12;  // measured 8192^3 / 65536x8192^2: 6 8 12 16 24 -> 12 best (profiles/r02_group_m.md)
-  p.l2_policy = g_l2_policy;
+  // Single problems: groups of 4 n-blocks with B resident (evict_last hint on B only), A streaming,
+  // odd groups sweeping m backwards.  Measured with ncu at 8192^3 (DRAM read 865 -> 785 MB) and
+  // 65536 x 8192 x 8192 (6.76 -> 5.76 GB), +1.3 % sustained TFLOP/s on the row-reduce bench (clock
+  // 1230 -> 1252 MHz under the power cap); larger resident groups thrash (64 MB of B: 7.6 GB).
+  // Batched problems keep m-grouping by 12 with no hints (a batch's operands are not reused).
+  const bool single = (L == 1);
+  p.raster = g_raster >= 0 ? g_raster : (single ? 1 : 0);
+  p.group_m = g_group_m > 0 ? g_group_m : (single ? 4 : 12);
+  p.l2_policy = g_l2_policy >= 0 ? g_l2_policy : (single ? 6 : 5);
+  p.serp = g_serp >= 0 ? g_serp : (single ? 1 : 0);
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
   p.act = act;
@@ -528,6 +535,19 @@ extern "C" int cy_gemm_trace_read(unsigned long long* out, int clear) {
   if (clear) {
     static unsigned long long zero[64 * 16] = {};
     cudaMemcpyToSymbol(g_gemm_trace, zero, sizeof(zero));
+  }
+  return static_cast<int>(e);
+}
+extern "C" int cy_gemm_etrace_read(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_gemm_etrace, sizeof(g_gemm_etrace)));
+}
+extern "C" int cy_gemm_ktrace_read(unsigned long long* ev, unsigned long long* gtime, int clear) {
+  cudaError_t e = cudaMemcpyFromSymbol(ev, g_gemm_ktrace, sizeof(g_gemm_ktrace));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(gtime, g_gemm_gtime, sizeof(g_gemm_gtime));
+  if (clear) {
+    static unsigned long long zero[1024 * 8] = {};
+    cudaMemcpyToSymbol(g_gemm_ktrace, zero, sizeof(g_gemm_ktrace));
+    cudaMemcpyToSymbol(g_gemm_gtime, zero, sizeof(g_gemm_gtime));
   }
   return static_cast<int>(e);
 }

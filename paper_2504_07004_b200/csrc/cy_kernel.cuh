@@ -54,7 +54,27 @@ __device__ unsigned long long g_gemm_trace[64 * 16];
   do {                                                                                     \
     if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) < 64) g_gemm_trace[(it) * 16 + (ev)] += (v);      \
   } while (0)
+// kernel-level events of every CTA (< 1024): clock64 per event, globaltimer at entry
+__device__ unsigned long long g_gemm_ktrace[1024 * 8];
+__device__ unsigned long long g_gemm_gtime[1024];
+#define CY_KT(ev)                                                            \
+  do {                                                                       \
+    if (blockIdx.x < 1024) g_gemm_ktrace[blockIdx.x * 8 + (ev)] = clock64(); \
+  } while (0)
+// epilogue chunk timeline of CTA CY_GEMM_TRACE_CTA, first tile: [warp][chunk][event]
+__device__ unsigned long long g_gemm_etrace[8 * 8 * 8];
+#define CY_ET(it, ew, q, ev)                                                                  \
+  do {                                                                                        \
+    if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) == 0 && (q) < 8 && lane == 0)                 \
+      g_gemm_etrace[((ew) * 8 + (q)) * 8 + (ev)] = clock64();                                 \
+  } while (0)
 #else
+#define CY_ET(it, ew, q, ev) \
+  do {                       \
+  } while (0)
+#define CY_KT(ev) \
+  do {            \
+  } while (0)
 #define CY_TR(it, ev) \
   do {                \
   } while (0)
@@ -76,7 +96,10 @@ struct Params {
   int m_blocks, n_blocks, k_blocks;
   int tiles;             // L * m_blocks * n_blocks
   int group_m;           // grouped rasterisation width (in m-blocks)
-  int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last, 4 last/first, 5 none
+  int l2_policy;         // TMA L2 hints for A/B: 0 normal/normal, 1 last/last, 2 first/first, 3 first/last,
+                         // 4 last/first, 5 none/none, 6 none/last, 7 last/none
+  int raster;            // 0: groups of group_m m-blocks, m fastest (A panels resident, B streams);
+                         // 1: groups of group_m n-blocks, n fastest (B panels resident, A streams)
   float* y;              // V_ROWREDUCE: y[M]
   int act;               // V_DUAL_GLU: 0 = SiLU, 1 = GELU (tanh form)
   int n_extra;           // number of extra D destinations in DstMaps (0 = D only)
@@ -89,6 +112,8 @@ struct Params {
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride;
                          // 2: one cluster per tile, no stealing (non-persistent)
+  int serp;              // 1: odd raster groups sweep the n-blocks in reverse (boustrophedon), so a
+                         //    group starts on the B panels its predecessor just read
 };
 
 // Extra destinations of every D tile (fused replication): tensor maps over this
@@ -133,6 +158,9 @@ struct Cfg {
   static constexpr int TMEM_COLS = pow2_cols(NUM_ACC_BUF * ACC_COLS);
   // Single-buffered accumulators (TMEM full) leave the epilogue exposed: give it two warps per
   // TMEM lane quarter (each takes every other 64-column chunk) and one staging buffer each.
+  // (Measured and not kept: the same split for double-buffered 256 x 256 tiles, which shortens the
+  // last tile's epilogue -- 2048^3 -1.6 % time, batched 64 x 1024^3 on 256 x 256 +3 %, 1-CTA
+  // 128 x 256 tiles +5..10 %: the 320-thread build caps registers at 168 and spills.)
   static constexpr int EPI_SPLIT = (NUM_ACC_BUF == 1) ? 2 : 1;
   static constexpr int EPI_WARPS = 4 * EPI_SPLIT;
   static constexpr int EPI_BUFS = (EPI_SPLIT == 2) ? 1 : 2;
@@ -173,6 +201,17 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& b, int&
   const int per_b = p.m_blocks * p.n_blocks;
   b = t / per_b;
   const int r = t - b * per_b;
+  if (p.raster == 1) {
+    const int group = p.group_m * p.m_blocks;
+    const int g = r / group;
+    const int first_n = g * p.group_m;
+    const int gn = min(p.n_blocks - first_n, p.group_m);
+    const int rg = r - g * group;
+    nb = first_n + rg % gn;
+    mb = rg / gn;
+    if (p.serp && (g & 1)) mb = p.m_blocks - 1 - mb;
+    return;
+  }
   const int group = p.group_m * p.n_blocks;
   const int g = r / group;
   const int first_m = g * p.group_m;
@@ -180,6 +219,7 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& b, int&
   const int rg = r - g * group;
   mb = first_m + rg % gm;
   nb = rg / gm;
+  if (p.serp && (g & 1)) nb = p.n_blocks - 1 - nb;
 }
 
 // Tile t and the k-block range [kb0, kb1) of split `sidx` (0 when not split).
@@ -227,6 +267,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                     const __grid_constant__ CUtensorMap tmD1, const Params p,
                     const __grid_constant__ DstMaps extra) {
   extern __shared__ uint8_t smem_raw[];
+#ifdef CY_GEMM_TRACE
+  if (threadIdx.x == 0) {
+    CY_KT(0);
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    if (blockIdx.x < 1024) g_gemm_gtime[blockIdx.x] = gt;
+  }
+#endif
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-B alignment
   const uint32_t sStage0 = base;
@@ -292,6 +340,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (CLr > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) CY_KT(1);
   // Everything above (barrier init, TMEM allocation, descriptor prefetch) overlapped the tail of
   // the previous kernel on this stream; global memory is touched only after it has completed.
   pdl_wait();
@@ -346,9 +395,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         case 2: pol_a = pol_b = policy_evict_first(); break;
         case 3: pol_a = policy_evict_first(); pol_b = policy_evict_last(); break;
         case 4: pol_a = policy_evict_last(); pol_b = policy_evict_first(); break;
+        case 6: pol_a = policy_evict_normal(); pol_b = policy_evict_last(); break;
+        case 7: pol_a = policy_evict_last(); pol_b = policy_evict_normal(); break;
         default: pol_a = pol_b = policy_evict_normal(); break;
       }
-      const bool hint = p.l2_policy != 5;
+      // no cache hint at all on an operand: measured, hint-free requests for the same lines from
+      // different SMs merge in L2
+      const bool hint_a = p.l2_policy != 5 && p.l2_policy != 6;
+      const bool hint_b = p.l2_policy != 5 && p.l2_policy != 7;
       uint32_t stage = 0, phase = 0;
       constexpr bool PAIR_TMA = (C::CG == 2);
       int t;
@@ -377,7 +431,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
           }
           const int k0 = kb * C::BK;
-          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint64_t pol) {
+          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint64_t pol, bool hint) {
             if constexpr (PAIR_TMA) {
               if (hint) tma_load_3d_pair(dst, tm, fb, c0, c1, b, pol);
               else tma_load_3d_pair_nohint(dst, tm, fb, c0, c1, b);
@@ -386,7 +440,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               else tma_load_3d_nohint(dst, tm, fb, c0, c1, b);
             }
           };
-          load(sA, &tmA, k0, am, pol_a);
+          load(sA, &tmA, k0, am, pol_a, hint_a);
 #pragma unroll
           for (int sl = 0; sl < C::NUM_B; ++sl) {
             // slot sl: dual -> B0 / B1 at the same columns; GEMM -> N sub-tile sl of B
@@ -401,7 +455,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                   tma_load_3d_pair_mc(dst, tmB, fb, cb + 64 * j, k0, b, uint16_t((1u << crank) | (1u << (crank ^ 2u))),
                                       pol_b);
               } else {
-                load(dst, tmB, cb + 64 * j, k0, pol_b);
+                load(dst, tmB, cb + 64 * j, k0, pol_b, hint_b);
               }
             }
           }
@@ -472,6 +526,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           mbar_wait(bFull + 8 * stage, phase);
           CY_TR_ADD(it, 7, clock64() - w0);
           if (kb == kb0) CY_TR(it, 5);
+          if (it == 0 && kb == kb0) CY_KT(2);
         };
 #else
         auto wait_full = [&](int) { mbar_wait(bFull + 8 * stage, phase); };
@@ -547,6 +602,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
         mma_commit<C::CG>(bTFull + 8 * buf, pair_mask);  // accumulator ready, both CTAs of the pair
         CY_TR(it, 6);
+        CY_KT(3);
       }
     } else if (lane == 0) {
       // peer CTA: the leader issues all MMAs; follow the tile schedule only
@@ -651,8 +707,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       };
       auto store_chunk = [&](int q) {  // staging slot -> D (and the replicas), next slot, next C
+        CY_ET(it, ew, q, 3);
         fence_proxy_async_smem();
         __syncwarp();
+        CY_ET(it, ew, q, 4);
         if (lane == 0 && !(kDebug & 4)) {  // (debug 4: timing experiment without the D stores)
           const int n0 = chunk_n0(nb, q);
           const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
@@ -660,6 +718,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
           bulk_commit();
           if (ew == 0 && q == NQ - 1) CY_TR(it, 12);
+          if (ew == 0 && q == NQ - 1) CY_KT(4);
         }
         if constexpr (C::EPI_BUFS == 2) slot ^= 1;
         if (cpf && q + 1 < NQ) fetch_c(nb, row0, b, q + 1, slot);  // next chunk's C
@@ -669,6 +728,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       // -> one RN cast -> swizzled staging -> TMA store
       auto emit = [&](int q, const uint32_t (&r)[64], const uint32_t (&gt)[C::GLU ? 64 : 1]) {
         slot_ready(q);
+        CY_ET(it, ew, q, 2);
         const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
@@ -699,6 +759,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                        pack2<C::DT>(f[6], f[7]));
         }
         store_chunk(q);
+        CY_ET(it, ew, q, 5);
       };
       auto load_chunk = [&](int q, uint32_t (&r)[64], uint32_t (&gt)[C::GLU ? 64 : 1]) {
         const int a = q / CPW;
@@ -819,7 +880,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       for (int q = 0; q < NQ; ++q) {
         uint32_t r[64];
         uint32_t gt[C::GLU ? 64 : 1];  // GLU: the gate operand (accumulator 1)
+        CY_ET(it, ew, q, 0);
         load_chunk(q, r, gt);
+        CY_ET(it, ew, q, 1);
         // The accumulator's last chunk is in registers: hand its TMEM columns back to the MMA
         // issuer before converting and storing it.
         if ((q + 1) % CPW == 0) release(q / CPW);
@@ -828,6 +891,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait_read<0>();  // shared staging must outlive the stores' reads
+#ifdef CY_GEMM_TRACE
+    if (ew == 0 && lane == 0) {
+      bulk_wait<0>();
+      CY_KT(5);
+    }
+#endif
   } else {
     // ------------------------------------------------------------------ row reduction (SIMT)
     const int q = warp & 3;
@@ -867,11 +936,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   }
 
   __syncwarp();
+  if (threadIdx.x == 0) CY_KT(6);
   tc_fence_before();
   if (CLr > 1) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::CG>(tmem_base, C::TMEM_COLS);
+    if (lane == 0) CY_KT(7);
   }
 }
 

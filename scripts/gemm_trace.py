@@ -5,7 +5,7 @@ gtrace CY_GEMM_TRACE=1).  Prints, per tile of CTA 0, the clock64 offsets (cycles
   Mw cycles the MMA thread waited on full stages;  Ma1 cycles waiting for accumulator 1 (split)
   E0 epilogue has the tile   E1 tfull seen   E2 acc0 released  E3 acc1 released  E4 last store issued
   Ew cycles the epilogue waited for a free staging slot / C tile
-Usage: python scripts/gemm_trace.py WORKLOAD   (batched | gemm8192 | batched-beta1)"""
+Usage: python scripts/gemm_trace.py WORKLOAD [cfg]  (batched | batched-beta1 | gemm<n>, e.g. gemm8192)"""
 import ctypes
 import os
 import sys
@@ -32,9 +32,10 @@ if w.startswith("batched"):
     beta = 1.0 if w == "batched-beta1" else 0.0
     run = lambda i: cy.gemm_batched(sets[i % 2][0], sets[i % 2][1], sets[i % 2][2], 1.0, beta, out=D)  # noqa
 else:
-    mk = lambda: torch.empty((8192, 8192), device="cuda", dtype=torch.float16).uniform_(-1, 1, generator=g)  # noqa
+    sz = int(w[4:])  # gemm<n>: n^3
+    mk = lambda: torch.empty((sz, sz), device="cuda", dtype=torch.float16).uniform_(-1, 1, generator=g)  # noqa
     sets = [(mk(), mk()) for _ in range(2)]
-    D = torch.empty((8192, 8192), device="cuda", dtype=torch.float16)
+    D = torch.empty((sz, sz), device="cuda", dtype=torch.float16)
     run = lambda i: cy.gemm(sets[i % 2][0], sets[i % 2][1], out=D)  # noqa
 buf = (ctypes.c_ulonglong * (64 * 16))()
 for i in range(20):
@@ -54,3 +55,17 @@ for t, r in enumerate(ev):
     rel = lambda j: (r[j] - t0) if r[j] else -1  # noqa
     print(f"{t:4d} {rel(0):6d} {rel(1):6d} {rel(2):6d} | {rel(3):6d} {rel(4):6d} {rel(5):6d} {rel(6):6d} {r[7]:6d} {r[14]:6d} | "
           f"{rel(8):6d} {rel(9):6d} {rel(10):6d} {rel(11):6d} {rel(12):6d} {r[13]:6d}")
+
+# epilogue chunk timeline of the first tile (general chunk loop only): per warp and chunk, cycles
+# (from the tile's tfull seen) at: load start, TMEM loaded, staging slot ready, store issued
+lib.cy_gemm_etrace_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+et = (ctypes.c_ulonglong * (8 * 8 * 8))()
+lib.cy_gemm_etrace_read(et)
+base = ev[0][9]
+if base and any(et[i] for i in range(512)):
+    print("epilogue chunks (cycles from tfull seen): warp q: load0 loaded slot st.shared-done fenced stored")
+    for w_ in range(8):
+        for q in range(8):
+            v = [et[(w_ * 8 + q) * 8 + e] for e in range(6)]
+            if any(v):
+                print(f"  w{w_} q{q}: " + " ".join(f"{(x - base) if x else -1:6d}" for x in v))
