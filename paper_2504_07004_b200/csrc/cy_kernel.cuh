@@ -840,38 +840,56 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         // beta == 0, single-buffered TMEM: both of this warp's chunks of an accumulator are loaded
         // and rounded (alpha*acc, one RN cast) into 16-bit pairs before the accumulator is handed
         // back, so the MMA issuer waits only for the TMEM loads.
-#pragma unroll 1
-        for (int a = 0; a < C::NUM_OUT; ++a) {
-          uint32_t pk[2][32];
+        auto load_pack = [&](int a, int g, uint32_t (&pk)[32]) {
+          uint32_t r[64];
+          if (has_k) {
+            const uint32_t ta = tmem_chunk(a, a * CPW + g);
+            tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            uint32_t r[64];
-            if (has_k) {
-              const uint32_t ta = tmem_chunk(a, a * CPW + g);
-              tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-              tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-              tmem_ld_wait();
-            } else {
-#pragma unroll
-              for (int i = 0; i < 64; ++i) r[i] = 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-              pk[g][i] = unit_alpha ? pack2<C::DT>(x0, x1) : pack2<C::DT>(x0 * p.alpha, x1 * p.alpha);
-            }
+            for (int i = 0; i < 64; ++i) r[i] = 0u;
           }
-          release(a);
-          if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            slot_ready(a * CPW + g);
-            const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
+          for (int i = 0; i < 32; ++i) {
+            const float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+            pk[i] = unit_alpha ? pack2<C::DT>(x0, x1) : pack2<C::DT>(x0 * p.alpha, x1 * p.alpha);
+          }
+        };
+        auto put = [&](int q, const uint32_t (&pk)[32]) {  // packed chunk -> staging -> TMA store
+          slot_ready(q);
+          const uint32_t row_addr = sE + slot * C::EPI_BUF_BYTES + lane * 128;
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-              st_shared_v4(row_addr + ((v ^ (lane & 7)) << 4), pk[g][4 * v], pk[g][4 * v + 1], pk[g][4 * v + 2],
-                           pk[g][4 * v + 3]);
-            store_chunk(a * CPW + g);
+          for (int v = 0; v < 8; ++v)
+            st_shared_v4(row_addr + ((v ^ (lane & 7)) << 4), pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+          store_chunk(q);
+        };
+        if constexpr (C::NUM_OUT == 2 && (kDebug & 8) == 0) {
+          // Two accumulators (tile N = 512 or a dual pair): accumulator 1 is handed back after only
+          // one store, not two -- chunk 0 of accumulator 0 goes out first, then accumulator 1 is
+          // loaded while its other chunk waits in registers (3 chunks held, 96 registers).
+          uint32_t pa[32], pb[32], pc[32];
+          load_pack(0, 0, pa);
+          load_pack(0, 1, pb);
+          release(0);
+          put(0, pa);
+          load_pack(1, 0, pa);
+          load_pack(1, 1, pc);
+          release(1);
+          put(1, pb);
+          put(CPW, pa);
+          put(CPW + 1, pc);
+        } else {
+#pragma unroll 1
+          for (int a = 0; a < C::NUM_OUT; ++a) {
+            uint32_t pk[2][32];
+            load_pack(a, 0, pk[0]);
+            load_pack(a, 1, pk[1]);
+            release(a);
+            if constexpr ((kDebug & 8) != 0) continue;  // timing experiment: TMEM loads only
+            put(a * CPW, pk[0]);
+            put(a * CPW + 1, pk[1]);
           }
         }
         continue;
