@@ -449,17 +449,23 @@ def oracle_unit_fn(kind, arrs):
 
 
 def oracle_calibrate(fn, m, nth):
-    """t(units) = fixed (operand decode) + units * per_unit, from two probes."""
+    """t(units) = fixed (operand decode) + units * per_unit, from two probes; the second probe grows
+    until its extra time stands clear of the run-to-run noise of the fixed part."""
     import numpy as np
 
     p1 = max(1, min(m // 2, max(2 * nth, 8)))
     t0 = time.perf_counter()
     fn(np.arange(p1))
     t1 = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    fn(np.arange(min(m, 2 * p1)))
-    t2 = time.perf_counter() - t0
-    per = max((t2 - t1) / max(1, min(m, 2 * p1) - p1), 1e-6)
+    p2 = min(m, 2 * p1)
+    while True:
+        t0 = time.perf_counter()
+        fn(np.arange(p2))
+        t2 = time.perf_counter() - t0
+        if t2 - t1 >= max(0.3, 0.2 * t1) or p2 >= m or t2 > 20.0:
+            break
+        p2 = min(m, 2 * p2)
+    per = max((t2 - t1) / max(1, p2 - p1), 1e-6)
     return max(t1 - per * p1, 0.0), per, p1
 
 
@@ -786,10 +792,10 @@ def reference_arm(args, rank, world):
     kind = case[0]
     fn, per_unit, m, unit = oracle_unit_fn(*case)
     fixed, per, p1 = oracle_calibrate(fn, m, nth)
-    # each step: >= 512 rows (batched: >= 1 GEMM), sized to ~4 s of CPU work so that the fixed
-    # per-call cost (operand decode) stays a small share, as in the cpu_baseline leg
+    # each step: >= 512 rows (batched: >= 1 GEMM), sized to ~10 s of CPU work -- the size of the
+    # cpu_baseline leg's sample (12 s), so the fixed per-call cost (operand decode) weighs the same
     floor = 1 if kind == "batched" else min(m, 512)
-    units_per_step = int(min(m, max(floor, (4.0 - fixed) / per)))
+    units_per_step = int(min(m, max(floor, (10.0 - fixed) / per)))
     steps = min(args.steps, 10)
     warm = min(args.warmup, 3)
     rng = np.random.default_rng(0)

@@ -14,7 +14,7 @@ ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
 sys.path.insert(0, ROOT)
 from paper_2504_07004_b200 import _lib  # noqa: E402
 
-_lib.use_library(os.path.join(ROOT, "build", "exp", "libcypress_gtrace.so"))
+_lib.use_library(os.path.join(ROOT, "build", "exp", os.environ.get("CY_TRACE_LIB", "libcypress_gtrace.so")))
 import torch  # noqa: E402
 
 import paper_2504_07004_b200 as cy  # noqa: E402
