@@ -141,6 +141,14 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_f16_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -286,20 +294,20 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
-  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_launch_dependents();  // (every thread: keeps the warps provably converged, see cy_ptx.cuh)
   if (warp >= 4 * NT) {
   // CS = 3: whole warpgroups re-balance registers at the top of each role's branch (softmax
   // warpgroups up to 208, the producer / MMA / spare warpgroup down to 72)
   if constexpr (CS == 3) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
   if (warp == W_PROD) {
     // ---------------------------------------------------------------- producer
-    if (lane == 0 && nall > 0) {
+    if (nall > 0) {  // all 32 lanes, converged; TMA and expect_tx are elect.sync-predicated
       const uint64_t pol = policy_evict_last();
       auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1) {
-        if (p.l2hint) tma_load_3d(dst, tm, bar, c0, c1, hb, pol);
-        else tma_load_3d_nohint(dst, tm, bar, c0, c1, hb);
+        if (p.l2hint) tma_load_3d_e(dst, tm, bar, c0, c1, hb, pol);
+        else tma_load_3d_nohint_e(dst, tm, bar, c0, c1, hb);
       };
-      mbar_arrive_expect_tx(bQFull, NT * TILE);
+      mbar_arrive_expect_tx_e(bQFull, NT * TILE);
       for (int t = 0; t < NT; ++t) {
         ld(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t);
         ld(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, q0 + BQ * t);
@@ -319,25 +327,25 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         const int k0 = j * BKV;
         if constexpr (CY_ATTN_PF > 0)
           if (j + CY_ATTN_PF >= 2) prefetch_kv(j + CY_ATTN_PF);
-        mbar_wait(bKEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
+        mbar_wait_w(bKEmpty + 8 * s, ((j >> 1) & 1) ^ 1);
         ATRACE(true, 8, 0, j);
 #ifdef CY_ATTN_DBG_NOLOAD
         // timing experiment only (invalid results): K/V tiles after the first ring fill are not reloaded
         if (j >= 4) {
-          mbar_arrive(bKFull + 8 * s);
+          mbar_arrive_e(bKFull + 8 * s);
           const int vs = j % VS;
-          mbar_wait(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
-          mbar_arrive(bVFull + 8 * vs);
+          mbar_wait_w(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
+          mbar_arrive_e(bVFull + 8 * vs);
           continue;
         }
 #endif
-        mbar_arrive_expect_tx(bKFull + 8 * s, TILE);
+        mbar_arrive_expect_tx_e(bKFull + 8 * s, TILE);
         ld(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0);
         ld(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0);
         const int vs = j % VS;
-        mbar_wait(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
+        mbar_wait_w(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
         ATRACE(true, 9, 0, j);
-        mbar_arrive_expect_tx(bVFull + 8 * vs, TILE);
+        mbar_arrive_expect_tx_e(bVFull + 8 * vs, TILE);
         ld(sV + vs * TILE, &tmV, bVFull + 8 * vs, 0, k0);
         ld(sV + vs * TILE + ATOM, &tmV, bVFull + 8 * vs, 64, k0);
       }
@@ -346,64 +354,65 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
     // ---------------------------------------------------------------- MMA issuer
     // Tensor-core order per block j: PV_0(j) | S_0(j+1) | PV_1(j) | S_1(j+1): while one softmax
     // warpgroup turns S_t into P_t, the tensor core runs the other tile's GEMMs (ping-pong).
-    if (lane == 0 && nall > 0) {
+    if (nall > 0) {  // all 32 lanes, converged; MMAs and commits are elect.sync-predicated
       constexpr uint32_t ID_S = idesc<DT, false>(), ID_PV = idesc<DT, true>();
       auto issue_s = [&](int t, int j) {
-        const uint32_t k = sK + (j & 1) * TILE, q = sQ + t * TILE;
+        // descriptors advance by adding (byte offset >> 4) to the start-address field (no carry: shared
+        // addresses stay below 256 KB), so each MMA costs one add per operand instead of a rebuild
+        const uint64_t kd0 = sdesc_sw128(sK + (j & 1) * TILE, 16, 1024), qd0 = sdesc_sw128(sQ + t * TILE, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
-          mma_f16<1>(tmem + TM_S + t * 128, sdesc_sw128(q + off, 16, 1024), sdesc_sw128(k + off, 16, 1024), ID_S,
-                     kk > 0);
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          mma_f16_e<1>(tmem + TM_S + t * 128, qd0 + off, kd0 + off, ID_S, kk > 0);
         }
-        mma_commit<1>(bSFull + 8 * t, 0);
+        mma_commit_e<1>(bSFull + 8 * t, 0);
       };
       auto issue_pv = [&](int t, int j) {
-        const uint32_t v = sV + (j % VS) * TILE;
+        const uint64_t vd0 = sdesc_sw128(sV + (j % VS) * TILE, ATOM, 1024);  // + kk * (2048 >> 4) per k16 step
         // O_t += P_t V_j: P_t read from TMEM (packed 16-bit pairs over S_t, 8 columns per k16 step);
         // S_t(j+1) is issued after this and tcgen05 ops execute in order, so it cannot clobber P_t.
         // CS = 3: the first four k16 steps (keys [0, 64), P columns [0, 32)) go as soon as that half
         // of P_t is in TMEM.
         constexpr int KK0 = (CS == 3) ? BKV / 32 : 0;
         if constexpr (CS == 3) {
-          mbar_wait(bPHalf + 8 * t, j & 1);
+          mbar_wait_w(bPHalf + 8 * t, j & 1);
           ATRACE(true, 4, t, j);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < KK0; ++kk)
-            mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8,
-                       sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV, (j | kk) != 0);
+            mma_f16_ts_e(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8, vd0 + kk * 128, ID_PV,
+                       (j | kk) != 0);
         }
-        mbar_wait(bPReady + 8 * t, j & 1);
+        mbar_wait_w(bPReady + 8 * t, j & 1);
         ATRACE(true, 5, t, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = KK0; kk < BKV / 16; ++kk)
-          mma_f16_ts(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8,
-                     sdesc_sw128(v + kk * 2048, ATOM, 1024), ID_PV, (j | kk) != 0);
-        mma_commit<1>(bOReady + 8 * t, 0);
+          mma_f16_ts_e(tmem + TM_O + t * 128, tmem + TM_S + t * 128 + P_COL + kk * 8, vd0 + kk * 128, ID_PV,
+                     (j | kk) != 0);
+        mma_commit_e<1>(bOReady + 8 * t, 0);
       };
-      mbar_wait(bQFull, 0);
-      mbar_wait(bKFull, 0);
+      mbar_wait_w(bQFull, 0);
+      mbar_wait_w(bKFull, 0);
       tc_fence_after();
       for (int t = 0; t < NT; ++t)
         if (nkv[t] > 0) issue_s(t, 0);
-      mma_commit<1>(bKEmpty, 0);  // K_0 consumed
+      mma_commit_e<1>(bKEmpty, 0);  // K_0 consumed
       for (int j = 0; j < nall; ++j) {
         const bool next = j + 1 < nall;
         // operands are awaited where they are first read: V_j before PV_0(j), K_{j+1} only before
         // S_0(j+1), so PV_0(j) runs while K_{j+1} is still landing
         bool k_ready = !next;
-        mbar_wait(bVFull + 8 * (j % VS), (j / VS) & 1);
+        mbar_wait_w(bVFull + 8 * (j % VS), (j / VS) & 1);
         ATRACE(true, 7, 0, j);
         tc_fence_after();
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           if (j < nkv[t]) issue_pv(t, j);
-          if (t == NT - 1) mma_commit<1>(bVEmpty + 8 * (j % VS), 0);  // V_j fully consumed
+          if (t == NT - 1) mma_commit_e<1>(bVEmpty + 8 * (j % VS), 0);  // V_j fully consumed
           if (next && j + 1 < nkv[t]) {
             if (!k_ready) {
-              mbar_wait(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
+              mbar_wait_w(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
               ATRACE(true, 10, 0, j + 1);
               tc_fence_after();
               k_ready = true;
@@ -413,10 +422,10 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
           }
         }
         if (!k_ready) {  // no S this iteration (causal tail): still consume the phase
-          mbar_wait(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
+          mbar_wait_w(bKFull + 8 * ((j + 1) & 1), ((j + 1) >> 1) & 1);
           tc_fence_after();
         }
-        if (next) mma_commit<1>(bKEmpty + 8 * ((j + 1) & 1), 0);  // K_{j+1} consumed
+        if (next) mma_commit_e<1>(bKEmpty + 8 * ((j + 1) & 1), 0);  // K_{j+1} consumed
       }
     }
   }

@@ -538,6 +538,9 @@ extern "C" int cy_gemm_trace_read(unsigned long long* out, int clear) {
   }
   return static_cast<int>(e);
 }
+extern "C" int cy_gemm_mtrace_read(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_gemm_mtrace, sizeof(g_gemm_mtrace)));
+}
 extern "C" int cy_gemm_etrace_read(unsigned long long* out) {
   return static_cast<int>(cudaMemcpyFromSymbol(out, g_gemm_etrace, sizeof(g_gemm_etrace)));
 }

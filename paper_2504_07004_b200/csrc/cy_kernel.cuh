@@ -52,7 +52,7 @@ __device__ unsigned long long g_gemm_trace[64 * 16];
   } while (0)
 #define CY_TR_ADD(it, ev, v)                                                               \
   do {                                                                                     \
-    if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) < 64) g_gemm_trace[(it) * 16 + (ev)] += (v);      \
+    if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) < 64 && (threadIdx.x & 31) == 0) g_gemm_trace[(it) * 16 + (ev)] += (v); \
   } while (0)
 // kernel-level events of every CTA (< 1024): clock64 per event, globaltimer at entry
 __device__ unsigned long long g_gemm_ktrace[1024 * 8];
@@ -60,6 +60,12 @@ __device__ unsigned long long g_gemm_gtime[1024];
 #define CY_KT(ev)                                                            \
   do {                                                                       \
     if (blockIdx.x < 1024) g_gemm_ktrace[blockIdx.x * 8 + (ev)] = clock64(); \
+  } while (0)
+// MMA issuer of CTA CY_GEMM_TRACE_CTA, first tile: [k-block][0 = stage full seen, 1 = its MMAs issued]
+__device__ unsigned long long g_gemm_mtrace[64 * 4];
+#define CY_MT(it, kb, ev)                                                                      \
+  do {                                                                                         \
+    if (blockIdx.x == CY_GEMM_TRACE_CTA && (it) == 0 && (kb) < 64) g_gemm_mtrace[(kb) * 4 + (ev)] = clock64(); \
   } while (0)
 // epilogue chunk timeline of CTA CY_GEMM_TRACE_CTA, first tile: [warp][chunk][event]
 __device__ unsigned long long g_gemm_etrace[8 * 8 * 8];
@@ -71,6 +77,9 @@ __device__ unsigned long long g_gemm_etrace[8 * 8 * 8];
 #else
 #define CY_ET(it, ew, q, ev) \
   do {                       \
+  } while (0)
+#define CY_MT(it, kb, ev) \
+  do {                    \
   } while (0)
 #define CY_KT(ev) \
   do {            \
@@ -344,7 +353,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   // Everything above (barrier init, TMEM allocation, descriptor prefetch) overlapped the tail of
   // the previous kernel on this stream; global memory is touched only after it has completed.
   pdl_wait();
-  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_launch_dependents();  // (every thread: a lane-0 branch here would leave the warps' convergence
+                            //  unprovable for ptxas, which then wraps each elected MMA / TMA in a loop)
 
   // ---------------------------------------------------------------- tile schedule
   // Tile i of this cluster: static -> cid + i*ncl; dynamic -> i == 0: own cluster's tile, i > 0:
@@ -362,33 +372,38 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     if (p.dyn == 2) return false;  // one tile per launched cluster, no stealing
     const int j = (i - 1) % C::SCHED_SLOTS;
     const uint32_t ph = ((i - 1) / C::SCHED_SLOTS) & 1;
-    mbar_wait(bSFull + 8 * j, ph);
     uint32_t ok, cx;
-    clc_decode(sResp + 16 * j, ok, cx);
-    if (warp_wide) __syncwarp();
-    if (!warp_wide || lane == 0) {
+    if (warp_wide) {  // converged warp: one elected lane releases the slot (no lane-0 branch)
+      mbar_wait_w(bSFull + 8 * j, ph);
+      clc_decode(sResp + 16 * j, ok, cx);
+      __syncwarp();
+      if (CLr > 1) mbar_arrive_cluster_e(mapa(bSEmpty + 8 * j, 0));
+      else mbar_arrive_e(bSEmpty + 8 * j);
+    } else {
+      mbar_wait(bSFull + 8 * j, ph);
+      clc_decode(sResp + 16 * j, ok, cx);
       if (CLr > 1) mbar_arrive_cluster(mapa(bSEmpty + 8 * j, 0));
       else mbar_arrive(bSEmpty + 8 * j);
     }
     t = static_cast<int>(cx) / CLr;
     return ok != 0;
   };
-  // Producer thread, at the start of its tile i: arm this CTA's slot for tile i+1 and (leader)
+  // Producer warp, at the start of its tile i: arm this CTA's slot for tile i+1 and (leader)
   // ask the hardware for the next pending cluster.
   auto sched_request = [&](int i) {
     if (p.dyn != 1) return;
     const int j = i % C::SCHED_SLOTS;
-    mbar_arrive_expect_tx(bSFull + 8 * j, 16);
+    mbar_arrive_expect_tx_e(bSFull + 8 * j, 16);
     if (crank == 0) {
-      mbar_wait(bSEmpty + 8 * j, ((i / C::SCHED_SLOTS) & 1) ^ 1);
-      if (CLr > 1) clc_try_cancel_multicast(sResp + 16 * j, bSFull + 8 * j);
-      else clc_try_cancel(sResp + 16 * j, bSFull + 8 * j);
+      mbar_wait_w(bSEmpty + 8 * j, ((i / C::SCHED_SLOTS) & 1) ^ 1);
+      if (CLr > 1) clc_try_cancel_multicast_e(sResp + 16 * j, bSFull + 8 * j);
+      else clc_try_cancel_e(sResp + 16 * j, bSFull + 8 * j);
     }
   };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer (TMA)
-    if (lane == 0) {
+    {  // all 32 lanes, converged; single-thread instructions are elect.sync-predicated (cy_ptx.cuh)
       uint64_t pol_a, pol_b;
       switch (p.l2_policy) {
         case 1: pol_a = pol_b = policy_evict_last(); break;
@@ -406,7 +421,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       uint32_t stage = 0, phase = 0;
       constexpr bool PAIR_TMA = (C::CG == 2);
       int t;
-      for (int i = 0; sched_next(i, t, false); ++i) {
+      for (int i = 0; sched_next(i, t, true); ++i) {
         CY_TR(i, 0);
         sched_request(i);
         int b, mb, nb, kb0, kb1;
@@ -414,30 +429,30 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const int am = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA;
         const int bn = nb * C::TILE_N + rank * C::BN_CTA;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(bEmpty + 8 * stage, phase ^ 1);
+          mbar_wait_w(bEmpty + 8 * stage, phase ^ 1);
           if (kb == kb0) CY_TR(i, 1);
           if (kb == kb1 - 1) CY_TR(i, 2);
           const uint32_t sA = sStage0 + stage * C::STAGE_BYTES;
           uint32_t fb = bFull + 8 * stage;
           if ((kDebug & 1) && (phase || i != 0)) {  // timing experiment: reuse stale stages
-            if (PAIR_TMA ? rank == 0 : true) mbar_arrive(fb);  // (MC == 1 only)
+            if (PAIR_TMA ? rank == 0 : true) mbar_arrive_e(fb);  // (MC == 1 only)
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
           if constexpr (PAIR_TMA) {
-            if (rank == 0) mbar_arrive_expect_tx(fb, C::STAGE_BYTES * 2);
+            if (rank == 0) mbar_arrive_expect_tx_e(fb, C::STAGE_BYTES * 2);
             fb = mapa(fb, leader);  // both CTAs of the pair count bytes on the leader's barrier
           } else {
-            mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+            mbar_arrive_expect_tx_e(fb, C::STAGE_BYTES);
           }
           const int k0 = kb * C::BK;
           auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint64_t pol, bool hint) {
             if constexpr (PAIR_TMA) {
-              if (hint) tma_load_3d_pair(dst, tm, fb, c0, c1, b, pol);
-              else tma_load_3d_pair_nohint(dst, tm, fb, c0, c1, b);
+              if (hint) tma_load_3d_pair_e(dst, tm, fb, c0, c1, b, pol);
+              else tma_load_3d_pair_nohint_e(dst, tm, fb, c0, c1, b);
             } else {
-              if (hint) tma_load_3d(dst, tm, fb, c0, c1, b, pol);
-              else tma_load_3d_nohint(dst, tm, fb, c0, c1, b);
+              if (hint) tma_load_3d_e(dst, tm, fb, c0, c1, b, pol);
+              else tma_load_3d_nohint_e(dst, tm, fb, c0, c1, b);
             }
           };
           load(sA, &tmA, k0, am, pol_a, hint_a);
@@ -452,8 +467,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               if constexpr (C::MC == 2) {
                 // every other atom: ours, multicast to us and our counterpart in the other pair
                 if (((sl * (C::BN_CTA / 64) + j) & 1) == int(pp))
-                  tma_load_3d_pair_mc(dst, tmB, fb, cb + 64 * j, k0, b, uint16_t((1u << crank) | (1u << (crank ^ 2u))),
-                                      pol_b);
+                  tma_load_3d_pair_mc_e(dst, tmB, fb, cb + 64 * j, k0, b, uint16_t((1u << crank) | (1u << (crank ^ 2u))),
+                                        pol_b);
               } else {
                 load(dst, tmB, cb + 64 * j, k0, pol_b, hint_b);
               }
@@ -465,7 +480,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // all 32 lanes, converged; the MMAs and commits are elect.sync-predicated
       uint32_t stage = 0, phase = 0;
       constexpr uint16_t kAllMask = uint16_t((1u << C::CL) - 1u);  // stage release: every CTA of the cluster
       const uint16_t pair_mask = uint16_t(0x3u << leader);          // this pair's two CTAs
@@ -482,8 +497,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           // apart (SBO); K advances 16 rows = 2048 B.
           const uint64_t bd = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
           const uint32_t acc = (kb != kfirst || kk != 0);
-          if constexpr (C::VAR == V_DUAL_SUM) mma_f16<C::CG>(d, ad, bd, C::IDESC, sl ? 1u : acc);
-          else mma_f16<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
+          if constexpr (C::VAR == V_DUAL_SUM) mma_f16_e<C::CG>(d, ad, bd, C::IDESC, sl ? 1u : acc);
+          else mma_f16_e<C::CG>(d + sl * C::BN, ad, bd, C::IDESC, acc);
         }
       };
       // both B slots of one k-block, interleaved per k16 step so the second MMA reuses the A
@@ -498,21 +513,21 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           const uint64_t bd1 = sdesc_sw128(sB + C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
           const uint32_t acc = (kb != kfirst || kk != 0);
           if constexpr (C::VAR == V_DUAL_SUM) {
-            mma_f16_col<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
-            mma_f16_col<C::CG, 2>(d, ad, bd1, C::IDESC, 1u);
+            mma_f16_col_e<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
+            mma_f16_col_e<C::CG, 2>(d, ad, bd1, C::IDESC, 1u);
           } else {
-            mma_f16_col<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
-            mma_f16_col<C::CG, 2>(d + C::BN, ad, bd1, C::IDESC, acc);
+            mma_f16_col_e<C::CG, 1>(d, ad, bd0, C::IDESC, acc);
+            mma_f16_col_e<C::CG, 2>(d + C::BN, ad, bd1, C::IDESC, acc);
           }
         }
       };
       auto release = [&](int st) {
         // frees the stage: in both CTAs of the pair (B multicast, MC == 2: in both pairs)
-        mma_commit<C::CG>(bEmpty + 8 * st, C::MC == 2 ? kAllMask : pair_mask);
-        if constexpr (C::REDUCE) mma_commit<C::CG>(bMDone + 8 * st, pair_mask);  // reducers may read it
+        mma_commit_e<C::CG>(bEmpty + 8 * st, C::MC == 2 ? kAllMask : pair_mask);
+        if constexpr (C::REDUCE) mma_commit_e<C::CG>(bMDone + 8 * st, pair_mask);  // reducers may read it
       };
       int t;
-      for (int it = 0; sched_next(it, t, false); ++it) {
+      for (int it = 0; sched_next(it, t, true); ++it) {
         const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
         const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
         const uint32_t d = tmem_base + buf * C::ACC_COLS;
@@ -521,22 +536,26 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         kfirst = kb0;
         CY_TR(it, 3);
 #ifdef CY_GEMM_TRACE
+        long long tr_mw = 0;  // full-barrier wait cycles of this tile (kept in a register: a global
+                              // read-modify-write per k-block would slow the traced CTA itself)
         auto wait_full = [&](int kb) {
           const long long w0 = clock64();
-          mbar_wait(bFull + 8 * stage, phase);
-          CY_TR_ADD(it, 7, clock64() - w0);
+          mbar_wait_w(bFull + 8 * stage, phase);
+          tr_mw += clock64() - w0;
           if (kb == kb0) CY_TR(it, 5);
           if (it == 0 && kb == kb0) CY_KT(2);
         };
 #else
-        auto wait_full = [&](int) { mbar_wait(bFull + 8 * stage, phase); };
+        auto wait_full = [&](int) { mbar_wait_w(bFull + 8 * stage, phase); };
 #endif
         if constexpr (!C::SPLIT) {
-          mbar_wait(bTEmpty + 8 * buf, bph ^ 1);
+          mbar_wait_w(bTEmpty + 8 * buf, bph ^ 1);
           CY_TR(it, 4);
           tc_fence_after();
           for (int kb = kb0; kb < kb1; ++kb) {
+            CY_MT(it, kb - kb0, 2);
             wait_full(kb);
+            CY_MT(it, kb - kb0, 0);
             tc_fence_after();
             if constexpr (C::NUM_B == 2) {
               if (p.a_reuse) issue_both(d, stage, kb);
@@ -544,12 +563,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             } else {
               issue(d, stage, 0, kb);
             }
+            CY_MT(it, kb - kb0, 1);
             release(stage);
+            CY_MT(it, kb - kb0, 3);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
         } else {
           // bTEmpty[a] = accumulator a drained by both CTAs' epilogues
-          mbar_wait(bTEmpty, bph ^ 1);
+          mbar_wait_w(bTEmpty, bph ^ 1);
           CY_TR(it, 4);
           tc_fence_after();
           bool acc1 = false;
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               continue;
             }
             issue(d, stage, 0, kb);
-            if (!acc1 && mbar_test_wait(bTEmpty + 8, bph ^ 1)) {
+            if (!acc1 && __any_sync(0xffffffffu, mbar_test_wait(bTEmpty + 8, bph ^ 1))) {
               acc1 = true;
               tc_fence_after();
             }
@@ -583,10 +604,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             } else if (held == C::STAGES) {  // every stage is held: wait for accumulator 1
 #ifdef CY_GEMM_TRACE
               const long long w1 = clock64();
-              mbar_wait(bTEmpty + 8, bph ^ 1);
+              mbar_wait_w(bTEmpty + 8, bph ^ 1);
               CY_TR_ADD(it, 14, clock64() - w1);
 #else
-              mbar_wait(bTEmpty + 8, bph ^ 1);
+              mbar_wait_w(bTEmpty + 8, bph ^ 1);
 #endif
               acc1 = true;
               tc_fence_after();
@@ -595,13 +616,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
           if (held) {
-            mbar_wait(bTEmpty + 8, bph ^ 1);
+            mbar_wait_w(bTEmpty + 8, bph ^ 1);
             tc_fence_after();
             flush();
           }
         }
-        mma_commit<C::CG>(bTFull + 8 * buf, pair_mask);  // accumulator ready, both CTAs of the pair
+        mma_commit_e<C::CG>(bTFull + 8 * buf, pair_mask);  // accumulator ready, both CTAs of the pair
         CY_TR(it, 6);
+#ifdef CY_GEMM_TRACE
+        CY_TR_ADD(it, 7, tr_mw);
+#endif
         CY_KT(3);
       }
     } else if (lane == 0) {

@@ -236,6 +236,89 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   return p;
 }
 
+
+// ---------------------------------------------------------------- warp-uniform issue (elect.sync)
+// The producer and MMA-issuer warps run their loops with all 32 lanes converged; each single-thread
+// instruction (TMA, tcgen05.mma / commit, expect_tx, try_cancel) is predicated on elect.sync inside
+// the same asm block.  ptxas then keeps the loop state and descriptors in uniform registers and
+// issues back-to-back UTCHMMA / UTMALDG, instead of wrapping every instruction of a lane-0 branch
+// in an ELECT / BRA.U.ANY loop fed through R2UR (measured ~60 cycles per MMA and ~370 per k-block
+// of loop overhead with the lane-0 form: the MMA issue, not the tensor core, bounded 128 x 64
+// tiles at ~20 % and 256 x 256 tiles at ~83 % of the tensor rate).
+#define CY_ELECT "elect.sync _|ep, 0xffffffff;\n\t@ep "
+// Warp-uniform wait: every lane polls until the phase completes (traps after ~2^28 polls).
+__device__ __forceinline__ void mbar_wait_w(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .u32 n;\n\tmov.u32 n, 0;\n"
+      "CY_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra CY_DONE;\n\t"
+      "add.u32 n, n, 1;\n\t"
+      "setp.lt.u32 p, n, 268435456;\n\t"
+      "@p bra CY_WAIT;\n\t"
+      "trap;\n"
+      "CY_DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_e(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_e(uint32_t bar_cluster) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT "mbarrier.arrive.shared::cluster.b64 _, [%0];\n\t}" ::"r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_e(uint32_t bar) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT "mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1, int c2,
+                                              uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" CY_ELECT
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_nohint_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1,
+                                                     int c2) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" CY_ELECT
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster, int c0,
+                                                   int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" CY_ELECT
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_nohint_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster,
+                                                          int c0, int c1, int c2) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" CY_ELECT
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_mc_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster, int c0,
+                                                      int c1, int c2, uint16_t cta_mask, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" CY_ELECT
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask), "l"(policy)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05 / TMEM
 template <int CG>
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
@@ -330,6 +413,65 @@ __device__ __forceinline__ void mma_commit(uint32_t bar, uint16_t mask) {
         : "memory");
 }
 
+
+template <int CG>
+__device__ __forceinline__ void mma_f16_e(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+template <int CG, int COL>
+__device__ __forceinline__ void mma_f16_col_e(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  static_assert(COL == 1 || COL == 2, "collector mode");
+  if constexpr (CG == 1 && COL == 1)
+    asm volatile(
+        "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+        "tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else if constexpr (CG == 1 && COL == 2)
+    asm volatile(
+        "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+        "tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else if constexpr (CG == 2 && COL == 1)
+    asm volatile(
+        "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, %4, 0;\n\t" CY_ELECT
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void mma_commit_e(uint32_t bar, uint16_t mask) {
+  if constexpr (CG == 1)
+    asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT
+                 "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+                 : "memory");
+  else
+    asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT
+                 "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+                 "h"(mask)
+                 : "memory");
+}
+
 // 32 lanes x 32 consecutive fp32 columns: thread t of the warp gets row (lane base + t).
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -361,6 +503,20 @@ __device__ __forceinline__ void clc_try_cancel_multicast(uint32_t resp, uint32_t
       "[%0], [%1];" ::"r"(resp),
       "r"(bar)
       : "memory");
+}
+
+__device__ __forceinline__ void clc_try_cancel_e(uint32_t resp, uint32_t bar) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT
+               "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];\n\t}" ::"r"(resp),
+               "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void clc_try_cancel_multicast_e(uint32_t resp, uint32_t bar) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT
+               "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.multicast::cluster::all.b128 "
+               "[%0], [%1];\n\t}" ::"r"(resp),
+               "r"(bar)
+               : "memory");
 }
 // Decode a response: ok = a cluster was cancelled (its work is ours), cx = its first CTA's x index.
 __device__ __forceinline__ void clc_decode(uint32_t resp, uint32_t& ok, uint32_t& cx) {

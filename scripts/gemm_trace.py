@@ -69,3 +69,16 @@ if base and any(et[i] for i in range(512)):
             v = [et[(w_ * 8 + q) * 8 + e] for e in range(6)]
             if any(v):
                 print(f"  w{w_} q{q}: " + " ".join(f"{(x - base) if x else -1:6d}" for x in v))
+
+# MMA issuer of the first tile (non-split accumulators only): per k-block, cycles from the tile's
+# first stage full to (stage full seen, its MMAs issued)
+lib.cy_gemm_mtrace_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+mt = (ctypes.c_ulonglong * 256)()
+lib.cy_gemm_mtrace_read(mt)
+if mt[0]:
+    b0 = mt[0]  # (event 0 of k-block 0)
+    print("MMA issuer per k-block (cycles from the first full seen): loop_top full_seen issued committed")
+    for kb in range(64):
+        if not mt[4 * kb]:
+            break
+        print(f"  kb {kb:2d}: " + " ".join(f"{mt[4 * kb + e] - b0:7d}" for e in (2, 0, 1, 3)))
