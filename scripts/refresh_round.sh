@@ -30,3 +30,8 @@ for w in batched dual rowreduce; do
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn -s 3 -c 1 -f -o $O/prof_${R}_attention \
   python bench.py --workload attention --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu_attn=$?"
+timeout 600 python scripts/attn_probe.py > $O/attn_probe.txt 2>&1; echo "attn_probe=$?"
+# summaries on the box; keep only the headline GEMM and attention reports (gpurun copies back <= 64 MiB)
+python scripts/ncu_summary.py gemm=$O/prof_${R}_gemm.ncu-rep batched=$O/prof_${R}_batched.ncu-rep dual=$O/prof_${R}_dual.ncu-rep \
+  rowreduce=$O/prof_${R}_rowreduce.ncu-rep attention=$O/prof_${R}_attention.ncu-rep > $O/ncu_summary.json 2>&1; echo "ncu_summary=$?"
+rm -f $O/prof_${R}_batched.ncu-rep $O/prof_${R}_dual.ncu-rep $O/prof_${R}_rowreduce.ncu-rep
