@@ -25,13 +25,14 @@ using cy::Params;
 // kernel menu
 struct KDesc {
   int var, dt, cg, bn, stages, threads, smem, mc;  // bn = output tile width (TILE_N); mc = pairs sharing B
+  int bn_cta;                                      // B columns per CTA per B slot (multiple of 64)
   const void* fn;
 };
 
 template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1, int MC = 1>
 KDesc kdesc() {
   using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB, MC>;
-  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, (const void*)&cy::cy_sm100_kernel<C>};
+  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, C::BN_CTA, (const void*)&cy::cy_sm100_kernel<C>};
 }
 
 // Shapes (cta_group, tile N, pairs per cluster) offered per variant; the GEMM menu defines the
@@ -87,6 +88,7 @@ const int g_group_m = env_int("CY_GROUP_M", 0);
 const int g_l2_policy = env_int("CY_L2_POLICY", -1);
 const int g_serp = env_int("CY_SERP", -1);
 const int g_raster = env_int("CY_RASTER", -1);
+const int g_b4d = env_int("CY_B4D", 1);
 // CY_SCHED: 0 = dynamic (cluster launch control) when there is more than one wave, 1 = static
 const int g_sched = [] {
   const char* e = std::getenv("CY_SCHED");
@@ -171,7 +173,7 @@ struct MapKey {
   const void* ptr;
   uint64_t cols, rows, batch, ld, stride;
   uint32_t box_c, box_r;
-  int dt, pad;
+  int dt, atoms;  // atoms > 0: 4-D map {64, rows, cols / 64, batch} with boxes of `atoms` 64-column atoms
   bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
 };
 struct MapKeyHash {
@@ -187,11 +189,11 @@ std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;  // bounded: cleared when it grows past 4096
 
 bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64_t rows, uint64_t batch,
-                uint64_t ld, uint64_t stride, uint32_t box_c, uint32_t box_r) {
+                uint64_t ld, uint64_t stride, uint32_t box_c, uint32_t box_r, uint32_t atoms = 0) {
   MapKey key;
   std::memset(&key, 0, sizeof(key));
   key.ptr = ptr; key.cols = cols; key.rows = rows; key.batch = batch; key.ld = ld; key.stride = stride;
-  key.box_c = box_c; key.box_r = box_r; key.dt = dt;
+  key.box_c = box_c; key.box_r = box_r; key.dt = dt; key.atoms = static_cast<int>(atoms);
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_maps.find(key);
@@ -200,14 +202,25 @@ bool encode_map(CUtensorMap* out, int dt, const void* ptr, uint64_t cols, uint64
       return true;
     }
   }
-  cuuint64_t dims[3] = {cols, rows, batch};
-  cuuint64_t strides[2] = {ld * 2, stride * 2};
-  cuuint32_t box[3] = {box_c, box_r, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
-  CUresult r = g_encode(&m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
-                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (atoms > 0) {  // {64 columns, rows, cols / 64 atoms, batch}; strides: row, 128 B per atom, batch
+    cuuint64_t dims[4] = {64, rows, cols / 64, batch};
+    cuuint64_t strides[3] = {ld * 2, 128, stride * 2};
+    cuuint32_t box[4] = {64, box_r, atoms, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = g_encode(&m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                 const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[3] = {cols, rows, batch};
+    cuuint64_t strides[2] = {ld * 2, stride * 2};
+    cuuint32_t box[3] = {box_c, box_r, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    r = g_encode(&m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                 const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) return false;
   *out = m;
   std::lock_guard<std::mutex> lk(g_map_mu);
@@ -393,16 +406,23 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   CUtensorMap tA, tB0, tB1, tC0, tC1, tD0, tD1;
   std::memset(&tA, 0, sizeof(CUtensorMap));
   tB0 = tB1 = tC0 = tC1 = tD0 = tD1 = tA;
-  auto enc = [&](CUtensorMap* out, Operand o, int64_t rows, int64_t cols, uint32_t bc, uint32_t br) {
+  auto enc = [&](CUtensorMap* out, Operand o, int64_t rows, int64_t cols, uint32_t bc, uint32_t br, uint32_t atoms = 0) {
     const int64_t stride = (L > 1) ? o.stride : rows * o.ld;
     return encode_map(out, dt, o.ptr, (uint64_t)cols, (uint64_t)rows, (uint64_t)L, (uint64_t)o.ld,
-                      (uint64_t)stride, bc, br);
+                      (uint64_t)stride, bc, br, atoms);
   };
+  // B as 4-D boxes of all the slot's atoms (one TMA op per slot) when every atom is whole
+  // (n % 64 == 0, so no box reads past a row) -- measured per-SM TMA rate 56 vs 35 B/clk for one
+  // 4-atom box vs four 2-D boxes (scripts/experiments/tma_stream.cu)
+  // (single-atom slots keep the 2-D form: measured 7.3 vs 7.6 us at 1024^3 on 128 x 64 tiles; the
+  // multi-atom slots gain 0.5-1.5 %: 2048^3 16.5 -> 16.2 us, 4096^3, batched)
+  const bool b4d = g_b4d && kd.mc == 1 && (n % 64) == 0 && kd.bn_cta >= 128;
+  const uint32_t b_atoms = b4d ? static_cast<uint32_t>(kd.bn_cta / 64) : 0;
   bool ok = true;
   if (k > 0) {
     ok = ok && enc(&tA, A, m, k, 64, 128);
-    ok = ok && enc(&tB0, B0, k, n, 64, 64);
-    if (B1.ptr) ok = ok && enc(&tB1, B1, k, n, 64, 64);
+    ok = ok && enc(&tB0, B0, k, n, 64, 64, b_atoms);
+    if (B1.ptr) ok = ok && enc(&tB1, B1, k, n, 64, 64, b_atoms);
   }
   const bool has_c = (beta != 0.0f);
   if (has_c) {
@@ -438,6 +458,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.group_m = g_group_m > 0 ? g_group_m : (single ? 4 : 12);
   p.l2_policy = g_l2_policy >= 0 ? g_l2_policy : (single ? 6 : 5);
   p.serp = g_serp >= 0 ? g_serp : (single ? 1 : 0);
+  p.b4d = b4d ? 1 : 0;
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
   p.act = act;

@@ -121,6 +121,8 @@ struct Params {
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride;
                          // 2: one cluster per tile, no stealing (non-persistent)
+  int b4d;               // 1: B (and B1) tensor maps are 4-D {64 cols, K, N/64 atoms, batch} (N % 64 == 0):
+                         //    one TMA op per B slot instead of one per 64-column atom
   int serp;              // 1: odd raster groups sweep the n-blocks in reverse (boustrophedon), so a
                          //    group starts on the B panels its predecessor just read
 };
@@ -461,6 +463,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             // slot sl: dual -> B0 / B1 at the same columns; GEMM -> N sub-tile sl of B
             const CUtensorMap* tmB = (C::DUAL && sl == 1) ? &tmB1 : &tmB0;
             const int cb = bn + (C::DUAL ? 0 : sl * C::BN);
+            if (C::MC == 1 && p.b4d) {  // all of the slot's 64-column atoms in one 4-D box (one TMA op)
+              const uint32_t dst = sA + C::A_BYTES + sl * C::B_BYTES;
+              if constexpr (PAIR_TMA) tma_load_4d_pair_e(dst, tmB, fb, 0, k0, cb / 64, b, pol_b, hint_b);
+              else tma_load_4d_e(dst, tmB, fb, 0, k0, cb / 64, b, pol_b, hint_b);
+              continue;
+            }
 #pragma unroll
             for (int j = 0; j < C::BN_CTA / 64; ++j) {
               const uint32_t dst = sA + C::A_BYTES + sl * C::B_BYTES + j * C::B_ATOM_BYTES;
