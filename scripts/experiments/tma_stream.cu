@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(32, 1) k(const __grid_constant__ CUtensorMap t
                                            int rows_total, unsigned long long* cyc, int br, int nb, int d3) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t base = (su32(sm) + 1023u) & ~1023u;
-  const uint32_t bars = base + 6 * 32768;
+  const uint32_t bars = base + 6 * 32768;  // (64 KB stages: 3)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -30,13 +30,15 @@ __global__ void __launch_bounds__(32, 1) k(const __grid_constant__ CUtensorMap t
                      "r"(((i - stages) / stages) & 1));
       }
       if (i < iters) {
-        asm volatile("{\n\t.reg .pred ep;\n\telect.sync _|ep, 0xffffffff;\n\t@ep mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bars + 8 * s), "r"(32768));
-        if (d3) {  // one 3-D box {64 cols, br rows, nb atoms}
+        asm volatile("{\n\t.reg .pred ep;\n\telect.sync _|ep, 0xffffffff;\n\t@ep mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bars + 8 * s), "r"(d3 >= 2 ? 65536 : 32768));
+        if (d3) {  // 3-D boxes {64 cols, 64 rows, atoms}
           const int row = ((grp * 4 + i) * 128) % rows_total;
-          asm volatile("{\n\t.reg .pred ep;\n\telect.sync _|ep, 0xffffffff;\n\t@ep cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n\t}" ::"r"(
-                           base + s * 32768),
-                       "l"(&tm), "r"(0), "r"(row), "r"(0), "r"(bars + 8 * s)
-                       : "memory");
+          const uint32_t ssz = d3 == 1 ? 32768 : 65536;
+          for (int bb = 0; bb < (d3 == 3 ? 2 : 1); ++bb)
+            asm volatile("{\n\t.reg .pred ep;\n\telect.sync _|ep, 0xffffffff;\n\t@ep cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n\t}" ::"r"(
+                             base + s * ssz + bb * 32768),
+                         "l"(&tm), "r"(0), "r"(row), "r"(bb * 4), "r"(bars + 8 * s)
+                         : "memory");
         }
         for (int b = 0; b < (d3 ? 0 : nb); ++b) {
           const int row = ((grp * 4 + i) * 128 + b * br) % rows_total;
@@ -68,28 +70,30 @@ int main() {
   const int smem = 6 * 32768 + 1024 + 256;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
-  auto mk3 = [&](CUtensorMap* tm) {  // {64 cols, rows, 8 atoms of 64 cols}: box {64, 64, 4} = 4 atoms x 64 rows
+  auto mk3 = [&](CUtensorMap* tm, int atoms3) {  // {64 cols, rows, 8 atoms of 64 cols}: box {64, 64, 4} = 4 atoms x 64 rows
     cuuint64_t dims[3] = {64, (cuuint64_t)rows, 8};
     cuuint64_t strides[2] = {(cuuint64_t)cols * 8 * 2, 128};
-    cuuint32_t box[3] = {64, 64, 4}, es[3] = {1, 1, 1};
+    cuuint32_t box[3] = {64, 64, (cuuint32_t)atoms3}, es[3] = {1, 1, 1};
     return cuTensorMapEncodeTiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
-  for (int cfg = 0; cfg < 3; ++cfg)
-    for (int stages : {4, 6}) for (int nct : {1, 148}) {
+  for (int cfg = 0; cfg < 5; ++cfg)
+    for (int stages : {3}) for (int nct : {1, 148}) {
       // cfg 0: four 2-D boxes 64 x 64 per 32 KB stage; 1: one 3-D box 64 x 64 x 4; 2: two 2-D boxes 64 x 128
       CUtensorMap tm;
       const int br = cfg == 2 ? 128 : 64, nb = cfg == 0 ? 4 : cfg == 2 ? 2 : 4, d3 = cfg == 1;
-      if (!(d3 ? mk3(&tm) : mk(&tm, br))) { printf("encode failed\n"); return 1; }
-      k<<<nct, 32, smem>>>(tm, 64, stages, 0, rows, cyc, br, nb, d3);
-      k<<<nct, 32, smem>>>(tm, iters, stages, 0, rows, cyc, br, nb, d3);
+      const int big = cfg >= 3;  // 64 KB stages
+      if (!(d3 || big ? mk3(&tm, cfg == 3 ? 8 : 4) : mk(&tm, br))) { printf("encode failed\n"); return 1; }
+      const int d3m = d3 ? 1 : cfg == 3 ? 2 : cfg == 4 ? 3 : 0;
+      k<<<nct, 32, smem>>>(tm, 64, stages, 0, rows, cyc, br, nb, d3m);
+      k<<<nct, 32, smem>>>(tm, iters, stages, 0, rows, cyc, br, nb, d3m);
       if (cudaDeviceSynchronize() != cudaSuccess) { printf("launch failed: %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
       std::vector<unsigned long long> h(nct);
       cudaMemcpy(h.data(), cyc, sizeof(unsigned long long) * nct, cudaMemcpyDeviceToHost);
       unsigned long long mx = 0; for (auto v : h) mx = v > mx ? v : mx;
-      const double per_sm = 32768.0 * iters / mx;
+      const double per_sm = (cfg >= 3 ? 65536.0 : 32768.0) * iters / mx;
       printf("cfg %d (%s), 32 KB stages %d, ctas %3d: %6.1f B/clk per SM, %7.0f B/clk total\n", cfg,
-             cfg == 0 ? "4 x 2-D 64x64" : cfg == 1 ? "1 x 3-D 64x64x4" : "2 x 2-D 64x128", stages, nct, per_sm, per_sm * nct);
+             cfg == 0 ? "4 x 2-D 64x64" : cfg == 1 ? "1 x 3-D 64x64x4" : cfg == 2 ? "2 x 2-D 64x128" : cfg == 3 ? "1 x 3-D 64x64x8 (64K)" : "2 x 3-D 64x64x4 (64K)", stages, nct, per_sm, per_sm * nct);
     }
   return 0;
 }
