@@ -26,28 +26,35 @@ using cy::Params;
 struct KDesc {
   int var, dt, cg, bn, stages, threads, smem, mc;  // bn = output tile width (TILE_N); mc = pairs sharing B
   int bn_cta;                                      // B columns per CTA per B slot (multiple of 64)
+  int bk;                                          // K per stage (64 or 128)
   const void* fn;
 };
 
-template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1, int MC = 1>
+template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1, int MC = 1, int BK = 64>
 KDesc kdesc() {
-  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB, MC>;
-  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, C::BN_CTA, (const void*)&cy::cy_sm100_kernel<C>};
+  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB, MC, BK>;
+  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, C::BN_CTA, BK,
+               (const void*)&cy::cy_sm100_kernel<C>};
 }
 
 // Shapes (cta_group, tile N, pairs per cluster) offered per variant; the GEMM menu defines the
 // public config ids.
-struct Shape { int cg, bn, mc; };
-constexpr Shape kGemmMenu[] = {{2, 256, 1}, {2, 128, 1}, {1, 256, 1}, {1, 128, 1}, {1, 64, 1}, {2, 512, 1}, {2, 512, 2}};
+struct Shape { int cg, bn, mc, bk; };
+// The narrow tiles (pair 256 x 128, single 128 x 64) stage K = 128 per k-block: with 24 KB stages
+// the per-SM TMA op rate, not bandwidth, bounded them (measured, graph replay: 1024^3 7.8 -> 6.7 us on
+// 128 x 64, 2048^3 22.1 -> 16.4 us on 256 x 128); the wide tiles keep K = 64 (K = 128 leaves them
+// 2-3 stages: 8192^3 715 -> 810 us on 256 x 256).
+constexpr Shape kGemmMenu[] = {{2, 256, 1, 64}, {2, 128, 1, 128}, {1, 256, 1, 64}, {1, 128, 1, 64}, {1, 64, 1, 128},
+                               {2, 512, 1, 64}, {2, 512, 2, 64}};
 constexpr int kNumGemmCfg = sizeof(kGemmMenu) / sizeof(kGemmMenu[0]);
 
 template <int DT>
 void add_all(std::vector<KDesc>& v) {
   v.push_back(kdesc<DT, 2, 256, 6, cy::V_GEMM>());
-  v.push_back(kdesc<DT, 2, 128, 8, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 2, 128, 4, cy::V_GEMM, 1, 1, 128>());
   v.push_back(kdesc<DT, 1, 256, 4, cy::V_GEMM>());
   v.push_back(kdesc<DT, 1, 128, 6, cy::V_GEMM>());
-  v.push_back(kdesc<DT, 1, 64, 8, cy::V_GEMM>());
+  v.push_back(kdesc<DT, 1, 64, 4, cy::V_GEMM, 1, 1, 128>());
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2>());
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2, 2>());
   v.push_back(kdesc<DT, 2, 256, 6, cy::V_ROWREDUCE>());
@@ -297,7 +304,7 @@ int active_clusters(DevState* st, int idx, int csize) {
 // Predicted time of one launch: waves x (tile area per SM) x (K + exposed epilogue) / efficiency.
 // `units` = tiles in flight (co-resident clusters; a split-K cluster works on one tile).
 double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k, int64_t L, int64_t units,
-                int splits = 1) {
+                int splits = 1, int bk = 64) {
   const int64_t bm = 128 * cg;
   const int64_t tiles = L * ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
   const int64_t waves = (tiles + units - 1) / units;
@@ -305,10 +312,10 @@ double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k,
   // (shared-memory operand bytes per MMA and L2 bytes per FLOP fall as the tile grows)
   double eff = 1.0;
   if (cg == 2 && bn == 512) eff = 1.25;  // 25 % fewer L2 bytes per FLOP: more clock under the power cap
-  if (cg == 2 && bn == 128) eff = 0.70;
+  if (cg == 2 && bn == 128) eff = (bk == 128) ? 0.84 : 0.70;
   if (cg == 1 && bn == 256) eff = 0.80;
   if (cg == 1 && bn == 128) eff = 0.60;
-  if (cg == 1 && bn == 64) eff = 0.40;
+  if (cg == 1 && bn == 64) eff = (bk == 128) ? 0.49 : 0.40;
   const int64_t kb = (k + 63) / 64;
   const int64_t kb_split = (kb + splits - 1) / splits;
   double kk = static_cast<double>(std::max<int64_t>(kb_split * 64, 64)) + (single_buf ? 128.0 : 0.0) + 128.0;
@@ -331,7 +338,7 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, DevStat
   const auto& mn = menu();
   Choice best;
   double best_cost = 0;
-  const int64_t kb = (k + 63) / 64;
+  int64_t kb = (k + 63) / 64;
   const int forced = use_forced ? g_forced.load() : -1;
   // splits that leave no split empty: S -> ceil(kb / ceil(kb / S))
   auto eff_splits = [&](int sp) {
@@ -341,8 +348,10 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, DevStat
   };
   for (size_t i = 0; i < mn.size(); ++i) {
     if (mn[i].var != var || mn[i].dt != dt) continue;
+    kb = (k + mn[i].bk - 1) / mn[i].bk;  // k-blocks of this config
     if (forced >= 0 && forced < kNumGemmCfg) {
-      if (!(mn[i].cg == kGemmMenu[forced].cg && mn[i].bn == kGemmMenu[forced].bn && mn[i].mc == kGemmMenu[forced].mc))
+      if (!(mn[i].cg == kGemmMenu[forced].cg && mn[i].bn == kGemmMenu[forced].bn && mn[i].mc == kGemmMenu[forced].mc &&
+            mn[i].bk == kGemmMenu[forced].bk))
         continue;
     } else if (mn[i].mc != 1) {
       continue;  // B-multicast clusters: only when forced (being evaluated)
@@ -360,7 +369,8 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, DevStat
       if (can_split && forced_splits > 0 && sp != eff_splits(std::min(forced_splits, s_hi))) continue;
       if (sp > 1 && splitk_ws_bytes(mn[i], m, n, L, sp) > ws_bytes) continue;
       const int cl = mn[i].cg * mn[i].mc * sp;
-      const double c = cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, active_clusters(st, static_cast<int>(i), cl), sp);
+      const double c =
+          cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, active_clusters(st, static_cast<int>(i), cl), sp, mn[i].bk);
       if (best.idx < 0 || c < best_cost) {
         best.idx = static_cast<int>(i);
         best.splits = sp;
@@ -418,11 +428,14 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   // multi-atom slots gain 0.5-1.5 %: 2048^3 16.5 -> 16.2 us, 4096^3, batched)
   const bool b4d = g_b4d && kd.mc == 1 && (n % 64) == 0 && kd.bn_cta >= 128;
   const uint32_t b_atoms = b4d ? static_cast<uint32_t>(kd.bn_cta / 64) : 0;
+  // K = 128 stages: A's two K-atoms in one 4-D box when every K-atom is whole (k % 64 == 0: a
+  // partial atom would read past K, and garbage times B's zero-filled rows could be NaN)
+  const bool a4d = kd.bk > 64 && (k % 64) == 0;
   bool ok = true;
   if (k > 0) {
-    ok = ok && enc(&tA, A, m, k, 64, 128);
-    ok = ok && enc(&tB0, B0, k, n, 64, 64, b_atoms);
-    if (B1.ptr) ok = ok && enc(&tB1, B1, k, n, 64, 64, b_atoms);
+    ok = ok && enc(&tA, A, m, k, 64, 128, a4d ? static_cast<uint32_t>(kd.bk / 64) : 0);
+    ok = ok && enc(&tB0, B0, k, n, 64, kd.bk, b_atoms);
+    if (B1.ptr) ok = ok && enc(&tB1, B1, k, n, 64, kd.bk, b_atoms);
   }
   const bool has_c = (beta != 0.0f);
   if (has_c) {
@@ -442,7 +455,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.alpha = alpha; p.beta = beta; p.has_c = has_c ? 1 : 0;
   p.m_blocks = (int)((m + bm - 1) / bm);
   p.n_blocks = (int)((n + kd.bn - 1) / kd.bn);
-  p.k_blocks = (int)((k + 63) / 64);
+  p.k_blocks = (int)((k + kd.bk - 1) / kd.bk);
   p.splits = ch.splits;
   p.kb_split = p.splits > 1 ? (p.k_blocks + p.splits - 1) / p.splits : p.k_blocks;
   p.ws = p.splits > 1 ? static_cast<float*>(ws) : nullptr;
@@ -459,6 +472,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.l2_policy = g_l2_policy >= 0 ? g_l2_policy : (single ? 6 : 5);
   p.serp = g_serp >= 0 ? g_serp : (single ? 1 : 0);
   p.b4d = b4d ? 1 : 0;
+  p.a4d = a4d ? 1 : 0;
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
   p.act = act;
@@ -603,7 +617,8 @@ cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int
   if (id < 0 || id >= kNumGemmCfg) return CY_ERR_INVALID_VALUE;
   const auto& mn = menu();
   for (const auto& k : mn)
-    if (k.var == cy::V_GEMM && k.cg == kGemmMenu[id].cg && k.bn == kGemmMenu[id].bn && k.mc == kGemmMenu[id].mc) {
+    if (k.var == cy::V_GEMM && k.cg == kGemmMenu[id].cg && k.bn == kGemmMenu[id].bn && k.mc == kGemmMenu[id].mc &&
+        k.bk == kGemmMenu[id].bk) {
       if (cta_group) *cta_group = k.cg;
       if (tile_m) *tile_m = 128 * k.cg * k.mc;
       if (tile_n) *tile_n = k.bn;
@@ -624,7 +639,8 @@ int cy_last_config(void) {
   if (idx < 0) return -1;
   const auto& k = menu()[idx];
   for (int i = 0; i < kNumGemmCfg; ++i)
-    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn && kGemmMenu[i].mc == k.mc) return i;
+    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn && kGemmMenu[i].mc == k.mc && kGemmMenu[i].bk == k.bk)
+      return i;
   return -1;
 }
 

@@ -121,6 +121,7 @@ struct Params {
   int dyn;               // 1: dynamic tile schedule (one cluster launched per tile, running clusters steal
                          //    pending ones with clusterlaunchcontrol.try_cancel); 0: static stride;
                          // 2: one cluster per tile, no stealing (non-persistent)
+  int a4d;               // 1 (BK = 128): A is a 4-D map {64, rows, K / 64, batch} (K % 64 == 0): one op per stage
   int b4d;               // 1: B (and B1) tensor maps are 4-D {64 cols, K, N/64 atoms, batch} (N % 64 == 0):
                          //    one TMA op per B slot instead of one per 64-column atom
   int serp;              // 1: odd raster groups sweep the n-blocks in reverse (boustrophedon), so a
@@ -136,7 +137,7 @@ struct DstMaps {
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1, int MC_ = 1>
+template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1, int MC_ = 1, int BK_ = 64>
 struct Cfg {
   static constexpr int DT = DT_;  // 0 = fp16, 1 = bf16
   static constexpr int CG = CG_;  // CTAs per MMA (tcgen05 cta_group)
@@ -154,7 +155,11 @@ struct Cfg {
   static constexpr int BM_CTA = 128;          // accumulator rows per CTA = TMEM lanes
   static constexpr int BM = BM_CTA * CG;      // MMA M = output tile height
   static constexpr int TILE_N = DUAL ? BN : NSUB * BN;  // output tile width
-  static constexpr int BK = 64;               // one 128-byte swizzle atom of K per stage
+  // K per stage: 64 (one 128-byte swizzle atom) or 128 (two K-atoms, 16 KB apart for A, one box
+  // each for A and every B slot: half the TMA ops per byte, which sets the per-SM TMA rate)
+  static constexpr int BK = BK_;
+  static constexpr int KAT = BK / 64;         // K-atoms per stage
+  static constexpr int A_ATOM = BM_CTA * 128;  // one 64-element K-atom of the CTA's A rows (16 KB)
   static constexpr int UMMA_K = 16;
   static constexpr int NUM_B = DUAL ? 2 : NSUB;  // B slots per stage
   static constexpr int NUM_ACC = (VAR == V_DUAL_PAIR || GLU) ? 2 : (VAR == V_DUAL_SUM ? 1 : NSUB);
@@ -195,6 +200,7 @@ struct Cfg {
   static constexpr bool SPLIT = (NUM_ACC_BUF == 1 && NUM_ACC == 2 && !GLU);
 
   static_assert(BN % 64 == 0 && BN_CTA % 64 == 0, "B is loaded in 64-column swizzle atoms");
+  static_assert(BK == 64 || (BK == 128 && MC == 1), "K per stage: 64, or 128 without B multicast");
   static_assert(BN >= 64 && BN <= 256, "tcgen05 kind::f16 N range");
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static_assert(NUM_ACC_BUF * ACC_COLS <= 512, "TMEM has 512 columns");
@@ -457,7 +463,15 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               else tma_load_3d_nohint_e(dst, tm, fb, c0, c1, b);
             }
           };
-          load(sA, &tmA, k0, am, pol_a, hint_a);
+          if constexpr (C::KAT == 1) {
+            load(sA, &tmA, k0, am, pol_a, hint_a);
+          } else if (p.a4d) {  // both K-atoms of A in one 4-D box {64, 128 rows, KAT, 1}
+            if constexpr (PAIR_TMA) tma_load_4d_pair_e(sA, &tmA, fb, 0, am, k0 / 64, b, pol_a, hint_a);
+            else tma_load_4d_e(sA, &tmA, fb, 0, am, k0 / 64, b, pol_a, hint_a);
+          } else {
+#pragma unroll
+            for (int a = 0; a < C::KAT; ++a) load(sA + a * C::A_ATOM, &tmA, k0 + 64 * a, am, pol_a, hint_a);
+          }
 #pragma unroll
           for (int sl = 0; sl < C::NUM_B; ++sl) {
             // slot sl: dual -> B0 / B1 at the same columns; GEMM -> N sub-tile sl of B
@@ -499,8 +513,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const uint32_t sB = sA + C::A_BYTES + sl * C::B_BYTES;
 #pragma unroll
         for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
-          // A: K-major SW128, 8-row groups 1024 B apart; K advances 32 B inside the atom.
-          const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
+          // A: K-major SW128, 8-row groups 1024 B apart; K advances 32 B inside the atom, K-atoms
+          // (BK = 128) A_ATOM apart.
+          const uint64_t ad = sdesc_sw128(sA + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024);
           // B: MN-major SW128, 64-column atoms B_ATOM_BYTES apart (LBO), 8-K-row groups 1024 B
           // apart (SBO); K advances 16 rows = 2048 B.
           const uint64_t bd = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const uint32_t sB = sA + C::A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
-          const uint64_t ad = sdesc_sw128(sA + kk * 32, 16, 1024);
+          const uint64_t ad = sdesc_sw128(sA + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024);
           const uint64_t bd0 = sdesc_sw128(sB + kk * 2048, C::B_ATOM_BYTES, 1024);
           const uint64_t bd1 = sdesc_sw128(sB + C::B_BYTES + kk * 2048, C::B_ATOM_BYTES, 1024);
           const uint32_t acc = (kb != kfirst || kk != 0);
@@ -961,16 +976,19 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         mbar_wait(bMDone + 8 * stage, phase);  // the tensor core has read this stage; it is still resident
         if (do_red) {
-          const uint32_t row_addr = sStage0 + stage * C::STAGE_BYTES + r * 128;
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {  // logical 16-B chunk v = K elements 8v..8v+7, in k order
-            uint32_t x[4];
-            ld_shared_v4(row_addr + ((v ^ (r & 7)) << 4), x[0], x[1], x[2], x[3]);
+          for (int a = 0; a < C::KAT; ++a) {  // K-atoms in k order
+            const uint32_t row_addr = sStage0 + stage * C::STAGE_BYTES + a * C::A_ATOM + r * 128;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = unpack2<C::DT>(x[e]);
-              acc += f.x;
-              acc += f.y;
+            for (int v = 0; v < 8; ++v) {  // logical 16-B chunk v = K elements 8v..8v+7, in k order
+              uint32_t x[4];
+              ld_shared_v4(row_addr + ((v ^ (r & 7)) << 4), x[0], x[1], x[2], x[3]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = unpack2<C::DT>(x[e]);
+                acc += f.x;
+                acc += f.y;
+              }
             }
           }
         }
