@@ -303,15 +303,13 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
     // ---------------------------------------------------------------- producer
     if (nall > 0) {  // all 32 lanes, converged; TMA and expect_tx are elect.sync-predicated
       const uint64_t pol = policy_evict_last();
-      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1) {
-        if (p.l2hint) tma_load_3d_e(dst, tm, bar, c0, c1, hb, pol);
-        else tma_load_3d_nohint_e(dst, tm, bar, c0, c1, hb);
+      // Q, K, V maps are 4-D {64, rows, 2 column atoms, batch*head}: a whole 128 x 128 tile (both
+      // 64-column SW128 atoms, ATOM bytes apart) is one TMA op
+      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t bar, int row) {
+        tma_load_4d_e(dst, tm, bar, 0, row, 0, hb, pol, p.l2hint != 0);
       };
       mbar_arrive_expect_tx_e(bQFull, NT * TILE);
-      for (int t = 0; t < NT; ++t) {
-        ld(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t);
-        ld(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, q0 + BQ * t);
-      }
+      for (int t = 0; t < NT; ++t) ld(sQ + t * TILE, &tmQ, bQFull, q0 + BQ * t);
       auto prefetch_kv = [&](int jb) {
         if (jb < nall) {
           tma_prefetch_3d(&tmK, 0, jb * BKV, hb);
@@ -340,14 +338,12 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         }
 #endif
         mbar_arrive_expect_tx_e(bKFull + 8 * s, TILE);
-        ld(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0);
-        ld(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0);
+        ld(sK + s * TILE, &tmK, bKFull + 8 * s, k0);
         const int vs = j % VS;
         mbar_wait_w(bVEmpty + 8 * vs, ((j / VS) & 1) ^ 1);
         ATRACE(true, 9, 0, j);
         mbar_arrive_expect_tx_e(bVFull + 8 * vs, TILE);
-        ld(sV + vs * TILE, &tmV, bVFull + 8 * vs, 0, k0);
-        ld(sV + vs * TILE + ATOM, &tmV, bVFull + 8 * vs, 64, k0);
+        ld(sV + vs * TILE, &tmV, bVFull + 8 * vs, k0);
       }
     }
   } else if (warp == W_MMA) {
@@ -896,9 +892,8 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == W_PROD && lane == 0) {
       // ---------------------------------------------------------------- producer
       const uint64_t pol = policy_evict_last();
-      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t b, int c0, int c1, int hb) {
-        if (p.l2hint) tma_load_3d(dst, tm, b, c0, c1, hb, pol);
-        else tma_load_3d_nohint(dst, tm, b, c0, c1, hb);
+      auto ld = [&](uint32_t dst, const CUtensorMap* tm, uint32_t b, int row, int hb) {  // 4-D maps: whole tile
+        tma_load_4d(dst, tm, b, 0, row, 0, hb, pol, p.l2hint != 0);
       };
       int g = 0;  // K/V blocks loaded so far (ring position across items)
       int it = 0;
@@ -910,20 +905,17 @@ __global__ void __launch_bounds__(384, 1)
         if (it > 0) mbar_wait(bQEmpty, (it - 1) & 1);  // the previous item's S MMAs have read Q
         mbar_arrive_expect_tx(bQFull, NT * TILE);
         for (int t = 0; t < NT; ++t) {
-          ld(sQ + t * TILE, &tmQ, bQFull, 0, qt * BQ * NT + BQ * t, hb);
-          ld(sQ + t * TILE + ATOM, &tmQ, bQFull, 64, qt * BQ * NT + BQ * t, hb);
+          ld(sQ + t * TILE, &tmQ, bQFull, qt * BQ * NT + BQ * t, hb);
         }
         for (int j = 0; j < nall; ++j, ++g) {
           const int s = g & 1;
           const int k0 = j * BKV;
           mbar_wait(bKEmpty + 8 * s, ((g >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(bKFull + 8 * s, TILE);
-          ld(sK + s * TILE, &tmK, bKFull + 8 * s, 0, k0, hb);
-          ld(sK + s * TILE + ATOM, &tmK, bKFull + 8 * s, 64, k0, hb);
+          ld(sK + s * TILE, &tmK, bKFull + 8 * s, k0, hb);
           mbar_wait(bVEmpty + 8 * s, ((g >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(bVFull + 8 * s, TILE);
-          ld(sV + s * TILE, &tmV, bVFull + 8 * s, 0, k0, hb);
-          ld(sV + s * TILE + ATOM, &tmV, bVFull + 8 * s, 64, k0, hb);
+          ld(sV + s * TILE, &tmV, bVFull + 8 * s, k0, hb);
         }
       }
     } else if (warp == W_MMA && lane == 0) {
@@ -1500,6 +1492,17 @@ std::mutex g_attr_mu;
 bool g_attr_set[64][6][2][4] = {};
 int g_sms[64] = {};
 
+// {64 columns, rows, 2 column atoms, batch*head} with 128-row boxes of both atoms (one TMA op per tile)
+bool make_map4(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh) {
+  cuuint64_t dims[4] = {64, rows, uint64_t(D) / 64, bh};
+  cuuint64_t strides[3] = {uint64_t(D) * 2, 128, rows * uint64_t(D) * 2};
+  cuuint32_t box[4] = {64, 128, uint32_t(D) / 64, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_encode(m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                  const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 bool make_map(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_c, uint32_t box_r,
               bool swizzle = true) {
   cuuint64_t dims[3] = {uint64_t(D), rows, bh};
@@ -1578,9 +1581,13 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   std::memset(&tK, 0, sizeof(tK));
   tV = tK;
   const bool o32 = kern == 2 && split == 4;  // 32-column output boxes, unswizzled staging
-  bool ok = make_map(&tQ, dt, Q, seq_q, bh, 64, 128) && make_map(&tO, dt, O, seq_q, bh, o32 ? 32 : 64, 32, !o32);
+  // the two-tile kernels (kern 1) load Q / K / V tiles as one 4-D box each; the pair kernel keeps 3-D maps
+  const bool four = (kern == 1);
+  bool ok = (four ? make_map4(&tQ, dt, Q, seq_q, bh) : make_map(&tQ, dt, Q, seq_q, bh, 64, 128)) &&
+            make_map(&tO, dt, O, seq_q, bh, o32 ? 32 : 64, 32, !o32);
   if (seq_k > 0)
-    ok = ok && make_map(&tK, dt, K, seq_k, bh, 64, kern == 2 ? 64 : 128) && make_map(&tV, dt, V, seq_k, bh, 64, 128);
+    ok = ok && (four ? make_map4(&tK, dt, K, seq_k, bh) && make_map4(&tV, dt, V, seq_k, bh)
+                     : make_map(&tK, dt, K, seq_k, bh, 64, kern == 2 ? 64 : 128) && make_map(&tV, dt, V, seq_k, bh, 64, 128));
   if (!ok) return CY_ERR_LAUNCH;
   Params p;
   p.sq = (int)seq_q;

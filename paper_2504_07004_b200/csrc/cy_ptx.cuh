@@ -319,6 +319,22 @@ __device__ __forceinline__ void tma_load_3d_pair_mc_e(uint32_t dst, const CUtens
       : "memory");
 }
 
+// 4-D box, single-thread form (callers in a lane-0 branch)
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1, int c2,
+                                            int c3, uint64_t policy, bool hint) {
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
 // 4-D boxes (B as {64 columns, K rows, 64-column atoms, batch}: all atoms of a slot in one TMA op)
 __device__ __forceinline__ void tma_load_4d_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1, int c2,
                                               int c3, uint64_t policy, bool hint) {
