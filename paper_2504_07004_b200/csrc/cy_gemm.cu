@@ -87,9 +87,16 @@ std::atomic<int> g_forced{-1};
 // CY_RASTER 0 = groups of CY_GROUP_M m-blocks (A panels resident, B streams), 1 = groups of
 // CY_GROUP_M n-blocks (B panels resident, A streams); CY_SERP=1 reverses the sweep of odd groups;
 // CY_L2_POLICY = TMA L2 eviction hints for A/B (see Params::l2_policy).
+// The knobs are read from the environment only in timing-experiment builds
+// (scripts/build_experiment.py NAME CY_TUNING_KNOBS=1); the product library always runs the defaults.
 int env_int(const char* name, int dflt) {
+#ifdef CY_TUNING_KNOBS
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
 }
 const int g_group_m = env_int("CY_GROUP_M", 0);
 const int g_l2_policy = env_int("CY_L2_POLICY", -1);
@@ -97,25 +104,13 @@ const int g_serp = env_int("CY_SERP", -1);
 const int g_raster = env_int("CY_RASTER", -1);
 const int g_b4d = env_int("CY_B4D", 1);
 // CY_SCHED: 0 = dynamic (cluster launch control) when there is more than one wave, 1 = static
-const int g_sched = [] {
-  const char* e = std::getenv("CY_SCHED");
-  return e ? std::atoi(e) : 0;
-}();
+const int g_sched = env_int("CY_SCHED", 0);
 // CY_PDL=0 disables programmatic dependent launch (tuning / debugging knob)
-const int g_pdl = [] {
-  const char* e = std::getenv("CY_PDL");
-  return e ? std::atoi(e) : 1;
-}();
+const int g_pdl = env_int("CY_PDL", 1);
 // CY_SLEEP_NS: epilogue wait backoff cap in ns (0 = spin); tuning knob
-const int g_sleep_ns = [] {
-  const char* e = std::getenv("CY_SLEEP_NS");
-  return e ? std::atoi(e) : 0;
-}();
+const int g_sleep_ns = env_int("CY_SLEEP_NS", 0);
 // CY_A_REUSE=0 disables the A-operand collector reuse across the two accumulators (tuning knob)
-const int g_a_reuse = [] {
-  const char* e = std::getenv("CY_A_REUSE");
-  return e ? std::atoi(e) : 1;
-}();
+const int g_a_reuse = env_int("CY_A_REUSE", 1);
 std::atomic<int> g_last{-1};
 std::atomic<int> g_last_splits{1};
 std::atomic<int64_t> g_launches{0};
@@ -164,10 +159,7 @@ cy_status_t device_state(int& dev, DevState*& st) {
 // TMA descriptors (3-D: columns, rows, batch), cached
 // CY_L2_PROMO: TMA L2 sector promotion (tuning knob): 0 none, 1 64B, 2 128B, 3 256B (default)
 CUtensorMapL2promotion promo() {
-  static const int v = [] {
-    const char* e = std::getenv("CY_L2_PROMO");
-    return e ? std::atoi(e) : 3;
-  }();
+  static const int v = env_int("CY_L2_PROMO", 3);
   switch (v) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
     case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;

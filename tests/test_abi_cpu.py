@@ -73,6 +73,18 @@ def test_product_build_has_no_experiment_switches():
     assert "p.debug" not in kern
 
 
+def test_product_build_reads_no_tuning_knobs():
+    """Tile-order / L2 / scheduling / attention-variant knobs are read from the environment only in
+    experiment builds (CY_TUNING_KNOBS, CY_ATTN_EXPERIMENTS): the product library carries none of
+    their names, so no environment variable can change what the product path runs."""
+    from paper_2504_07004_b200 import build
+
+    data = open(build.build(), "rb").read()
+    for knob in (b"CY_GROUP_M", b"CY_RASTER", b"CY_SERP", b"CY_L2_POLICY", b"CY_B4D", b"CY_SCHED", b"CY_PDL",
+                 b"CY_SLEEP_NS", b"CY_A_REUSE", b"CY_L2_PROMO", b"CY_ATTN_KERNEL", b"CY_ATTN_CS", b"CY_ATTN_EMU"):
+        assert knob not in data, knob
+
+
 def test_library_is_sm100a_and_uses_tcgen05():
     """The cubin inside the .so is sm_100a and contains tcgen05 MMA / TMA / TMEM loads."""
     import shutil
