@@ -27,25 +27,38 @@ struct KDesc {
   int var, dt, cg, bn, stages, threads, smem, mc;  // bn = output tile width (TILE_N); mc = pairs sharing B
   int bn_cta;                                      // B columns per CTA per B slot (multiple of 64)
   int bk;                                          // K per stage (64 or 128)
+  int mx;                                          // 1: 2 x 2 multicast cluster of 128 x bn CTA tiles
   const void* fn;
+  int ct_m() const { return mx ? 256 : 128 * cg * mc; }  // cluster tile rows
+  int ct_n() const { return mx ? 2 * bn : bn; }          // cluster tile columns
+  int csize() const { return mx ? 4 : cg * mc; }         // CTAs per cluster (before split-K)
 };
 
-template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1, int MC = 1, int BK = 64>
+template <int DT, int CG, int BN, int ST, int VAR, int NSUB = 1, int MC = 1, int BK = 64, int MX = 0>
 KDesc kdesc() {
-  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB, MC, BK>;
-  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, C::BN_CTA, BK,
+  using C = cy::Cfg<DT, CG, BN, ST, VAR, NSUB, MC, BK, MX>;
+  return KDesc{VAR, DT, CG, C::TILE_N, ST, C::THREADS, C::SMEM_BYTES, MC, C::BN_CTA, BK, MX,
                (const void*)&cy::cy_sm100_kernel<C>};
 }
 
 // Shapes (cta_group, tile N, pairs per cluster) offered per variant; the GEMM menu defines the
 // public config ids.
-struct Shape { int cg, bn, mc, bk; };
+struct Shape { int cg, bn, mc, bk, mx; };
 // The narrow tiles (pair 256 x 128, single 128 x 64) stage K = 128 per k-block: with 24 KB stages
 // the per-SM TMA op rate, not bandwidth, bounded them (measured, graph replay: 1024^3 7.8 -> 6.7 us on
 // 128 x 64, 2048^3 22.1 -> 16.4 us on 256 x 128); the wide tiles keep K = 64 (K = 128 leaves them
 // 2-3 stages: 8192^3 715 -> 810 us on 256 x 256).
-constexpr Shape kGemmMenu[] = {{2, 256, 1, 64}, {2, 128, 1, 128}, {1, 256, 1, 64}, {1, 128, 1, 64}, {1, 64, 1, 128},
-                               {2, 512, 1, 64}, {2, 512, 2, 64}};
+// Experiment build only (CY_GEMM_MX): config 7, the 128 x 64 K = 128 tile in a 2 x 2 cluster that
+// multicasts A along N and B along M, so each CTA issues half of its operand bytes.  Bit-exact on
+// the whole GEMM suite, but not faster (graph replay: 1024^3 7.4 vs 7.0 us on config 4, 2048^3 and
+// 4096^3 on par with config 4): the narrow tiles are bound by the latency of the bytes each SM
+// receives, which multicast does not reduce.
+constexpr Shape kGemmMenu[] = {{2, 256, 1, 64, 0}, {2, 128, 1, 128, 0}, {1, 256, 1, 64, 0}, {1, 128, 1, 64, 0},
+                               {1, 64, 1, 128, 0}, {2, 512, 1, 64, 0}, {2, 512, 2, 64, 0}
+#ifdef CY_GEMM_MX
+                               , {1, 64, 1, 128, 1}
+#endif
+};
 constexpr int kNumGemmCfg = sizeof(kGemmMenu) / sizeof(kGemmMenu[0]);
 
 template <int DT>
@@ -57,6 +70,9 @@ void add_all(std::vector<KDesc>& v) {
   v.push_back(kdesc<DT, 1, 64, 4, cy::V_GEMM, 1, 1, 128>());
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2>());
   v.push_back(kdesc<DT, 2, 256, 4, cy::V_GEMM, 2, 2>());
+#ifdef CY_GEMM_MX
+  v.push_back(kdesc<DT, 1, 64, 4, cy::V_GEMM, 1, 1, 128, 1>());
+#endif
   v.push_back(kdesc<DT, 2, 256, 6, cy::V_ROWREDUCE>());
   v.push_back(kdesc<DT, 2, 128, 8, cy::V_ROWREDUCE>());
   v.push_back(kdesc<DT, 1, 128, 6, cy::V_ROWREDUCE>());
@@ -103,6 +119,9 @@ const int g_l2_policy = env_int("CY_L2_POLICY", -1);
 const int g_serp = env_int("CY_SERP", -1);
 const int g_raster = env_int("CY_RASTER", -1);
 const int g_b4d = env_int("CY_B4D", 1);
+const int g_d_policy = env_int("CY_D_POLICY", 0);  // L2 policy of the D stores (0 none, 1 first, 2 last)
+const int g_c_pf = env_int("CY_C_PF", 0);  // epilogue C tiles prefetched into L2 during the main loop
+const int g_pf_dist = env_int("CY_PF_DIST", 0);  // batched L2 prefetch distance in problems (0 = off)
 // CY_SCHED: 0 = dynamic (cluster launch control) when there is more than one wave, 1 = static
 const int g_sched = env_int("CY_SCHED", 0);
 // CY_PDL=0 disables programmatic dependent launch (tuning / debugging knob)
@@ -343,14 +362,14 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, DevStat
     kb = (k + mn[i].bk - 1) / mn[i].bk;  // k-blocks of this config
     if (forced >= 0 && forced < kNumGemmCfg) {
       if (!(mn[i].cg == kGemmMenu[forced].cg && mn[i].bn == kGemmMenu[forced].bn && mn[i].mc == kGemmMenu[forced].mc &&
-            mn[i].bk == kGemmMenu[forced].bk))
+            mn[i].bk == kGemmMenu[forced].bk && mn[i].mx == kGemmMenu[forced].mx))
         continue;
-    } else if (mn[i].mc != 1) {
-      continue;  // B-multicast clusters: only when forced (being evaluated)
+    } else if (mn[i].mc != 1 || mn[i].mx) {
+      continue;  // multicast clusters: only when forced (being evaluated)
     }
     const int acc_cols = ((var == cy::V_DUAL_PAIR || var == cy::V_DUAL_GLU) ? 2 : 1) * mn[i].bn;
     const int single = acc_cols * 2 > 512;
-    const bool can_split = var == cy::V_GEMM && mn[i].mc == 1 && mn[i].bn <= 256;  // one accumulator (NSUB 1)
+    const bool can_split = var == cy::V_GEMM && mn[i].mc == 1 && mn[i].mx == 0 && mn[i].bn <= 256;  // one accumulator (NSUB 1)
     if (!can_split && forced_splits > 1) continue;  // a requested split needs a splittable kernel
     // split-K clusters: cta_group x splits <= 8 CTAs (portable cluster size)
     const int s_cap = 8 / mn[i].cg;
@@ -360,7 +379,7 @@ Choice pick(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, DevStat
       if (eff_splits(sp) != sp) continue;  // same k-block ranges as a smaller count
       if (can_split && forced_splits > 0 && sp != eff_splits(std::min(forced_splits, s_hi))) continue;
       if (sp > 1 && splitk_ws_bytes(mn[i], m, n, L, sp) > ws_bytes) continue;
-      const int cl = mn[i].cg * mn[i].mc * sp;
+      const int cl = mn[i].csize() * sp;
       const double c =
           cfg_cost(mn[i].cg, mn[i].bn, single, m, n, k, L, active_clusters(st, static_cast<int>(i), cl), sp, mn[i].bk);
       if (best.idx < 0 || c < best_cost) {
@@ -402,7 +421,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   const int idx = ch.idx;
   if (idx < 0) return CY_ERR_INTERNAL;
   const KDesc& kd = menu()[idx];
-  const int bm = 128 * kd.cg * kd.mc;  // rows per cluster tile
+  const int bm = kd.ct_m();  // rows per cluster tile
   const int bn_cta = kd.bn / kd.cg;
 
   CUtensorMap tA, tB0, tB1, tC0, tC1, tD0, tD1;
@@ -418,15 +437,16 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   // 4-atom box vs four 2-D boxes (scripts/experiments/tma_stream.cu)
   // (single-atom slots keep the 2-D form: measured 7.3 vs 7.6 us at 1024^3 on 128 x 64 tiles; the
   // multi-atom slots gain 0.5-1.5 %: 2048^3 16.5 -> 16.2 us, 4096^3, batched)
-  const bool b4d = g_b4d && kd.mc == 1 && (n % 64) == 0 && kd.bn_cta >= 128;
+  const bool b4d = g_b4d && kd.mc == 1 && !kd.mx && (n % 64) == 0 && kd.bn_cta >= 128;
   const uint32_t b_atoms = b4d ? static_cast<uint32_t>(kd.bn_cta / 64) : 0;
   // K = 128 stages: A's two K-atoms in one 4-D box when every K-atom is whole (k % 64 == 0: a
   // partial atom would read past K, and garbage times B's zero-filled rows could be NaN)
-  const bool a4d = kd.bk > 64 && (k % 64) == 0;
+  // (MX: each CTA loads one K-atom of A and one 64-row half of the B stage -- 3-D maps, 64-row B boxes)
+  const bool a4d = kd.bk > 64 && (k % 64) == 0 && !kd.mx;
   bool ok = true;
   if (k > 0) {
     ok = ok && enc(&tA, A, m, k, 64, 128, a4d ? static_cast<uint32_t>(kd.bk / 64) : 0);
-    ok = ok && enc(&tB0, B0, k, n, 64, kd.bk, b_atoms);
+    ok = ok && enc(&tB0, B0, k, n, 64, kd.mx ? 64 : kd.bk, b_atoms);
     if (B1.ptr) ok = ok && enc(&tB1, B1, k, n, 64, kd.bk, b_atoms);
   }
   const bool has_c = (beta != 0.0f);
@@ -446,7 +466,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.M = (int)m; p.N = (int)n; p.K = (int)k; p.L = (int)L;
   p.alpha = alpha; p.beta = beta; p.has_c = has_c ? 1 : 0;
   p.m_blocks = (int)((m + bm - 1) / bm);
-  p.n_blocks = (int)((n + kd.bn - 1) / kd.bn);
+  p.n_blocks = (int)((n + kd.ct_n() - 1) / kd.ct_n());
   p.k_blocks = (int)((k + kd.bk - 1) / kd.bk);
   p.splits = ch.splits;
   p.kb_split = p.splits > 1 ? (p.k_blocks + p.splits - 1) / p.splits : p.k_blocks;
@@ -465,6 +485,18 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.serp = g_serp >= 0 ? g_serp : (single ? 1 : 0);
   p.b4d = b4d ? 1 : 0;
   p.a4d = a4d ? 1 : 0;
+  // Batched: prefetch the operands of the problem pf_dist ahead into L2 (each problem's A and B
+  // spans, padding between rows included; off for single problems and K = 0)
+  p.pf_dist = (L > 1 && k > 0) ? g_pf_dist : 0;
+  p.pf_a = static_cast<const char*>(A.ptr);
+  p.pf_b = static_cast<const char*>(B0.ptr);
+  p.pf_a_stride = A.stride * 2;
+  p.pf_b_stride = B0.stride * 2;
+  p.pf_a_bytes = ((m - 1) * A.ld + k) * 2 / 16 * 16;
+  p.pf_b_bytes = ((k - 1) * B0.ld + n) * 2 / 16 * 16;
+  if (B1.ptr) p.pf_dist = 0;
+  p.c_pf = g_c_pf;
+  p.d_policy = g_d_policy;
   p.sleep_ns = g_sleep_ns;
   p.a_reuse = g_a_reuse;
   p.act = act;
@@ -472,7 +504,7 @@ cy_status_t launch(int var, int dt, int64_t m, int64_t n, int64_t k, int64_t L, 
   p.y = y;
 
   if (!ensure_attr(st, idx)) return CY_ERR_LAUNCH;
-  const int csize = kd.cg * kd.mc * p.splits;  // split-K: the splits of a tile form one cluster
+  const int csize = kd.csize() * p.splits;  // split-K: the splits of a tile form one cluster
   if (csize > 8) return CY_ERR_INTERNAL;
   const int units = active_clusters(st, idx, csize);
   // More tiles than co-resident clusters: launch one cluster per tile and let running clusters
@@ -610,10 +642,10 @@ cy_status_t cy_config_info(int id, int* cta_group, int* tile_m, int* tile_n, int
   const auto& mn = menu();
   for (const auto& k : mn)
     if (k.var == cy::V_GEMM && k.cg == kGemmMenu[id].cg && k.bn == kGemmMenu[id].bn && k.mc == kGemmMenu[id].mc &&
-        k.bk == kGemmMenu[id].bk) {
+        k.bk == kGemmMenu[id].bk && k.mx == kGemmMenu[id].mx) {
       if (cta_group) *cta_group = k.cg;
-      if (tile_m) *tile_m = 128 * k.cg * k.mc;
-      if (tile_n) *tile_n = k.bn;
+      if (tile_m) *tile_m = k.ct_m();
+      if (tile_n) *tile_n = k.ct_n();
       if (stages) *stages = k.stages;
       return CY_OK;
     }
@@ -631,7 +663,8 @@ int cy_last_config(void) {
   if (idx < 0) return -1;
   const auto& k = menu()[idx];
   for (int i = 0; i < kNumGemmCfg; ++i)
-    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn && kGemmMenu[i].mc == k.mc && kGemmMenu[i].bk == k.bk)
+    if (kGemmMenu[i].cg == k.cg && kGemmMenu[i].bn == k.bn && kGemmMenu[i].mc == k.mc && kGemmMenu[i].bk == k.bk &&
+        kGemmMenu[i].mx == k.mx)
       return i;
   return -1;
 }
@@ -645,8 +678,8 @@ cy_status_t cy_last_kernel_info(int* variant, int* cta_group, int* tile_m, int* 
   const KDesc& k = menu()[idx];
   if (variant) *variant = k.var;
   if (cta_group) *cta_group = k.cg;
-  if (tile_m) *tile_m = 128 * k.cg * k.mc;
-  if (tile_n) *tile_n = k.bn;
+  if (tile_m) *tile_m = k.ct_m();
+  if (tile_n) *tile_n = k.ct_n();
   if (stages) *stages = k.stages;
   if (threads) *threads = k.threads;
   if (smem_bytes) *smem_bytes = k.smem;

@@ -126,6 +126,17 @@ struct Params {
                          //    one TMA op per B slot instead of one per 64-column atom
   int serp;              // 1: odd raster groups sweep the n-blocks in reverse (boustrophedon), so a
                          //    group starts on the B panels its predecessor just read
+  // Batched L2 prefetch (pf_dist > 0): the CTA (pair leader) running tile r of problem b prefetches
+  // slice r (of m_blocks * n_blocks) of problem b + pf_dist's A and B spans into L2, so the tiles
+  // of that problem find their operands in L2 instead of waiting on HBM.
+  int pf_dist;
+  int d_policy;          // L2 policy of the D stores: 0 none, 1 evict_first, 2 evict_last
+  int c_pf;              // beta != 0: each epilogue warp prefetches its chunks' C tiles into L2 when it
+                         // learns its next tile (during that tile's main loop)
+  const char* pf_a;      // A of problem 0 (span: pf_a_bytes from pf_a + b * pf_a_stride)
+  const char* pf_b;
+  long long pf_a_stride, pf_b_stride;
+  long long pf_a_bytes, pf_b_bytes;
 };
 
 // Extra destinations of every D tile (fused replication): tensor maps over this
@@ -137,7 +148,7 @@ struct DstMaps {
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1, int MC_ = 1, int BK_ = 64>
+template <int DT_, int CG_, int BN_, int STAGES_, int VAR_, int NSUB_ = 1, int MC_ = 1, int BK_ = 64, int MX_ = 0>
 struct Cfg {
   static constexpr int DT = DT_;  // 0 = fp16, 1 = bf16
   static constexpr int CG = CG_;  // CTAs per MMA (tcgen05 cta_group)
@@ -149,7 +160,13 @@ struct Cfg {
   // of its B atoms and multicasts them to the CTA at the same position in the other pair, so a
   // 512 x TILE_N cluster tile reads B from L2 once (SURVEY a4 "cluster TMA multicast").
   static constexpr int MC = MC_;
-  static constexpr int CL = CG * MC;          // cluster size
+  // MX = 1: a 2 x 2 cluster of single CTAs (cta_group::1, K = 128 per stage) whose cluster tile is
+  // 256 x 2*BN: the two CTAs on the same rows each load one K-atom of the A stage and multicast it to
+  // both, the two CTAs on the same columns each load one 64-row K half of the B stage and multicast
+  // it to both, so every CTA issues half of its operand bytes (the per-SM TMA feed, not the tensor
+  // core, bounds the narrow tiles of few-tile problems)
+  static constexpr int MX = MX_;
+  static constexpr int CL = MX ? 4 : CG * MC;  // cluster size
   static constexpr bool DUAL = (VAR == V_DUAL_PAIR || VAR == V_DUAL_SUM || VAR == V_DUAL_GLU);
   static constexpr bool GLU = (VAR == V_DUAL_GLU);
   static constexpr int BM_CTA = 128;          // accumulator rows per CTA = TMEM lanes
@@ -189,7 +206,7 @@ struct Cfg {
   static constexpr int NUM_WARPS = THREADS / 32;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   // split-K across the CTAs (pairs) of a cluster: plain GEMM tiles with one accumulator
-  static constexpr bool SPLITTABLE = (VAR == V_GEMM && MC == 1 && NSUB == 1);
+  static constexpr bool SPLITTABLE = (VAR == V_GEMM && MC == 1 && NSUB == 1 && MX == 0);
   static_assert(24 * STAGES + 232 + 8 * EPI_WARPS <= BAR_BYTES, "barrier region");
   // Row-reduce: the reducer warps learn that their CTA's A stage is in shared memory from a
   // second tcgen05.commit (bMDone, multicast to both CTAs of a pair) issued after the MMAs that
@@ -201,6 +218,11 @@ struct Cfg {
 
   static_assert(BN % 64 == 0 && BN_CTA % 64 == 0, "B is loaded in 64-column swizzle atoms");
   static_assert(BK == 64 || (BK == 128 && MC == 1), "K per stage: 64, or 128 without B multicast");
+  static_assert(MX == 0 || (CG == 1 && MC == 1 && BK == 128 && NSUB == 1 && VAR == V_GEMM && BN == 64),
+                "2 x 2 multicast cluster: single-CTA GEMM tiles of 128 x 64 with K = 128 stages");
+  // cluster tile (rows x columns) and the scheduler's block sizes
+  static constexpr int CT_M = MX ? 2 * BM : BM * MC;
+  static constexpr int CT_N = MX ? 2 * TILE_N : TILE_N;
   static_assert(BN >= 64 && BN <= 256, "tcgen05 kind::f16 N range");
   static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of dynamic shared memory");
   static_assert(NUM_ACC_BUF * ACC_COLS <= 512, "TMEM has 512 columns");
@@ -320,6 +342,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const uint32_t pp = (C::MC == 2) ? crank / C::CG : 0u;        // pair index in the cluster (MC == 2)
   const int sidx = (SPL > 1) ? int(crank / C::CG) : 0;          // split index (split-K)
   const uint32_t leader = crank & ~uint32_t(C::CG - 1);         // this pair's MMA leader
+  // MX: position in the 2 x 2 cluster (rm along M, rn along N); offsets of this CTA's tile in the
+  // cluster tile
+  const int rm = C::MX ? int(crank & 1u) : 0, rn = C::MX ? int(crank >> 1) : 0;
+  const int row_off = C::MX ? rm * C::BM : int(pp) * C::BM + int(rank) * C::BM_CTA;
+  const int col_off = C::MX ? rn * C::TILE_N : 0;
   const int cid = blockIdx.x / CLr;
   const int ncl = gridDim.x / CLr;
 
@@ -333,7 +360,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(bFull + 8 * s, 1);
-      mbar_init(bEmpty + 8 * s, C::MC + C::RED_WARPS);  // MMA commit of every pair reading it
+      mbar_init(bEmpty + 8 * s, (C::MX ? 4 : C::MC) + C::RED_WARPS);  // MMA commit of every pair reading it
       if (C::REDUCE) mbar_init(bMDone + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -434,8 +461,25 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         sched_request(i);
         int b, mb, nb, kb0, kb1;
         unit_coords(p, t, sidx, b, mb, nb, kb0, kb1);
-        const int am = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA;
-        const int bn = nb * C::TILE_N + rank * C::BN_CTA;
+        if (p.pf_dist > 0 && crank == 0 && b + p.pf_dist < p.L) {
+          // this tile's slice of problem b + pf_dist's operands (16-B granules)
+          const int per_b = p.m_blocks * p.n_blocks;
+          const int r = t - b * per_b;
+          const int bb = b + p.pf_dist;
+          auto pf = [&](const char* base, long long stride, long long bytes) {
+            const long long gran = bytes >> 4;
+            const long long g0 = gran * r / per_b, g1 = gran * (r + 1) / per_b;
+            const char* a = base + bb * stride + (g0 << 4);
+            for (long long g = g0; g < g1; g += (1ll << 20)) {  // <= 16 MB per op
+              const long long n16 = min(g1 - g, 1ll << 20);
+              bulk_prefetch_l2_e(a + ((g - g0) << 4), uint32_t(n16 << 4));
+            }
+          };
+          pf(p.pf_a, p.pf_a_stride, p.pf_a_bytes);
+          pf(p.pf_b, p.pf_b_stride, p.pf_b_bytes);
+        }
+        const int am = mb * C::CT_M + row_off;
+        const int bn = nb * C::CT_N + col_off + rank * C::BN_CTA;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_w(bEmpty + 8 * stage, phase ^ 1);
           if (kb == kb0) CY_TR(i, 1);
@@ -454,6 +498,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             mbar_arrive_expect_tx_e(fb, C::STAGE_BYTES);
           }
           const int k0 = kb * C::BK;
+          if constexpr (C::MX) {
+            // A: K-atom rn of the stage, to both CTAs on these rows; B: K rows [64 rm, 64 rm + 64) of
+            // the stage, to both CTAs on these columns (every CTA's expect_tx above counts all
+            // STAGE_BYTES landing in it)
+            tma_load_3d_mc_e(sA + rn * C::A_ATOM, &tmA, fb, k0 + 64 * rn, am, b, uint16_t(0x5u << rm), pol_a, hint_a);
+            tma_load_3d_mc_e(sA + C::A_BYTES + rm * (64 * 128), &tmB0, fb, bn, k0 + 64 * rm, b, uint16_t(0x3u << (2 * rn)),
+                             pol_b, hint_b);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint64_t pol, bool hint) {
             if constexpr (PAIR_TMA) {
               if (hint) tma_load_3d_pair_e(dst, tm, fb, c0, c1, b, pol);
@@ -546,7 +600,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       };
       auto release = [&](int st) {
         // frees the stage: in both CTAs of the pair (B multicast, MC == 2: in both pairs)
-        mma_commit_e<C::CG>(bEmpty + 8 * st, C::MC == 2 ? kAllMask : pair_mask);
+        if constexpr (C::MX) mma_commit_mc_e(bEmpty + 8 * st, kAllMask);  // all four CTAs feed every stage
+        else mma_commit_e<C::CG>(bEmpty + 8 * st, C::MC == 2 ? kAllMask : pair_mask);
         if constexpr (C::REDUCE) mma_commit_e<C::CG>(bMDone + 8 * st, pair_mask);  // reducers may read it
       };
       int t;
@@ -675,10 +730,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     const uint32_t sE = sEpi + ew * C::EPI_BUFS * C::EPI_BUF_BYTES;
     const uint32_t cbar = bCBar + 8 * ew;
     const uint64_t pol = policy_evict_normal();
+    const uint64_t dpol = p.d_policy == 1 ? policy_evict_first() : policy_evict_last();
     uint32_t slot = 0, cphase = 0;
     auto chunk_col = [&](int q) { return (C::EPI_SPLIT == 2 ? half : 0) + (q % CPW) * C::EPI_SPLIT; };
     // column of chunk q in the output; C/D maps of chunk q
-    auto chunk_n0 = [&](int nb, int q) { return nb * C::TILE_N + (C::DUAL ? 0 : (q / CPW) * C::BN) + 64 * chunk_col(q); };
+    auto chunk_n0 = [&](int nb, int q) {
+      return nb * C::CT_N + col_off + (C::DUAL ? 0 : (q / CPW) * C::BN) + 64 * chunk_col(q);
+    };
     auto chunk_c = [&](int q) { return (C::VAR == V_DUAL_PAIR && q / CPW == 1) ? &tmC1 : &tmC0; };
     auto chunk_d = [&](int q) { return (C::VAR == V_DUAL_PAIR && q / CPW == 1) ? &tmD1 : &tmD0; };
     // lane 0: wait until slot `s` may be overwritten (the store that last used it has read it) and
@@ -700,7 +758,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const bool has_k = kb1 > kb0;
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
-      const int row0 = mb * C::BM * C::MC + pp * C::BM + rank * C::BM_CTA + 32 * q4;
+      const int row0 = mb * C::CT_M + row_off + 32 * q4;
+      if (p.has_c && p.c_pf && lane == 0) {  // C of every chunk this warp will read, into L2
+#pragma unroll 1
+        for (int q = cpf ? 1 : 0; q < NQ; ++q) tma_prefetch_3d(chunk_c(q), chunk_n0(nb, q), row0, b);
+      }
       if (cpf) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
       if (ew == 0 && lane == 0) CY_TR(it, 8);
       if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
@@ -761,7 +823,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         if (lane == 0 && !(kDebug & 4)) {  // (debug 4: timing experiment without the D stores)
           const int n0 = chunk_n0(nb, q);
           const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
-          tma_store_3d(chunk_d(q), sb, n0, row0, b);
+          if (p.d_policy) tma_store_3d_hint(chunk_d(q), sb, n0, row0, b, dpol);
+          else tma_store_3d(chunk_d(q), sb, n0, row0, b);
           for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
           bulk_commit();
           if (ew == 0 && q == NQ - 1) CY_TR(it, 12);

@@ -163,6 +163,9 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int c0, i
                "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// L2 prefetch of `bytes` contiguous bytes (16-B aligned address and size; no shared memory, no
+// completion): warms L2 ahead of later TMA loads of the same lines
+// (warp-uniform call: one elected lane issues it)
 // CTA-pair form: data lands in this CTA's shared memory, completion bytes are counted on
 // `bar_cluster`, a barrier of either CTA of the pair (we use the leader's).
 __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster,
@@ -204,6 +207,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, uint32_t src
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(tm)),
                "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// the same with an L2 cache policy on the written lines
+__device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap* tm, uint32_t src, int c0, int c1, int c2,
+                                                  uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -261,6 +272,12 @@ __device__ __forceinline__ void mbar_wait_w(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2_e(const void* gptr, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT "cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(
+                   reinterpret_cast<uint64_t>(gptr)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx_e(uint32_t bar, uint32_t bytes) {
   asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
                "r"(bytes)
@@ -317,6 +334,26 @@ __device__ __forceinline__ void tma_load_3d_pair_mc_e(uint32_t dst, const CUtens
       ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;\n\t}" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask), "l"(policy)
       : "memory");
+}
+
+// Single-CTA load multicast to every CTA of `cta_mask` (same shared offsets; each destination's
+// barrier at offset `bar` counts the bytes landing in it)
+__device__ __forceinline__ void tma_load_3d_mc_e(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1,
+                                                 int c2, uint16_t cta_mask, uint64_t policy, bool hint) {
+  if (hint)
+    asm volatile(
+        "{\n\t.reg .pred ep;\n\t" CY_ELECT
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred ep;\n\t" CY_ELECT
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask)
+        : "memory");
 }
 
 // 4-D box, single-thread form (callers in a lane-0 branch)
@@ -522,6 +559,14 @@ __device__ __forceinline__ void mma_commit_e(uint32_t bar, uint16_t mask) {
                  "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
                  "h"(mask)
                  : "memory");
+}
+
+// cta_group::1 commit whose arrival is multicast to the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc_e(uint32_t bar, uint16_t mask) {
+  asm volatile("{\n\t.reg .pred ep;\n\t" CY_ELECT
+               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+               "h"(mask)
+               : "memory");
 }
 
 // 32 lanes x 32 consecutive fp32 columns: thread t of the warp gets row (lane base + t).

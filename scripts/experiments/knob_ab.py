@@ -1,7 +1,8 @@
 """A/B of the library's environment tuning knobs (read once at load, so one process per setting).
     python scripts/experiments/knob_ab.py REPS WORKLOADS 'CY_PF=0' 'CY_PF=8' 'CY_PF=8 CY_SERP=1' ...
 WORKLOADS: comma list of batched, batched1 (beta=1), batched16 (L2-resident 16 x 1024^3), g8192, rr65536, g4096, g16384.
-Settings run interleaved, REPS rounds; prints us/launch and TFLOP/s per (setting, workload)."""
+Settings run interleaved, REPS rounds, on build/exp/libcypress_knobs.so
+(scripts/build_experiment.py knobs CY_TUNING_KNOBS=1); prints us/launch and TFLOP/s per (setting, workload)."""
 import os
 import subprocess
 import sys
@@ -11,6 +12,11 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     import torch
 
     import paper_2504_07004_b200 as cy
+    from paper_2504_07004_b200 import _lib
+
+    # the product library reads no knobs: use the CY_TUNING_KNOBS experiment build
+    _lib.use_library(os.environ.get("CY_KNOBS_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "..",
+                                                                 "build", "exp", "libcypress_knobs.so")))
 
     g = torch.Generator(device="cuda").manual_seed(0)
     h = torch.float16
