@@ -64,6 +64,11 @@ using namespace cy;
 #ifndef CY_ATTN_PF
 #define CY_ATTN_PF 0
 #endif
+// CY_ATTN_SPEC: the CS = 3 softmax takes group 0's exponentials against the running max while it
+// reduces the row max (the block is redone in the rare case a row's max grows past the lazy bound)
+#ifndef CY_ATTN_SPEC
+#define CY_ATTN_SPEC 1
+#endif
 // CY_ATTN_TRACE (timing experiments only, never in the product build): clock64() stamps of one
 // CTA's per-block events, read back with cy_attn_trace()
 #ifdef CY_ATTN_TRACE
@@ -641,11 +646,78 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
           tmem_ld_32x32b_x32(tS + 64 * g + 32, *reinterpret_cast<uint32_t(*)[32]>(&vrow[g][32]));
         }
         tmem_ld_wait();
+        ATRACE(tr, 11, t, j);
 #pragma unroll
         for (int g = 0; g < 2; ++g) fix(vrow[g], g);
-        // balanced 3-ary tree (depth 5, every level independent ops) instead of 8 serial chains
         auto sc = [&](int k) { return __uint_as_float(vrow[k >> 6][k & 63]); };
         auto max3 = [](float a, float b, float c) { return fmaxf(fmaxf(a, b), c); };
+        bool have_max = false;
+        if constexpr (CY_ATTN_SPEC != 0) {
+          if (j > 0) {
+            // Speculative pass (j > 0): take group 0's exponentials against the running max m -- the
+            // value P has whenever no row's max grows past the lazy bound (m_new == m below) -- and
+            // reduce the row max in 8 chains between them, so the max costs no time of its own.
+            // No row grows (the usual case): group 1 follows against m and the block is done, with
+            // the same P, sums and order as the path below.  Some row grows: the max is kept and
+            // the path below redoes the block against m_new.
+            if constexpr (CY_ATTN_PP == 1) pp_wait(j);
+            const float ms = (m == -INFINITY) ? 0.f : m;
+            const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+            const float2 ms2 = make_float2(-ms, -ms);
+            float2 sm4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+            float c8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c8[u] = -INFINITY;
+            uint32_t pk[32];
+            auto exp_pair = [&](int g, int e) {
+              const float2 x = ffma2(make_float2(__uint_as_float(vrow[g][2 * e]), __uint_as_float(vrow[g][2 * e + 1])),
+                                     sc2, ms2);
+              float2 pe;
+              pe.x = ex2(x.x);
+              pe.y = ex2(x.y);
+              sm4[e & 3] = fadd2(sm4[e & 3], pe);
+              pk[e] = pack2<DT>(pe.x, pe.y);
+            };
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              exp_pair(0, e);
+              c8[e & 3] = max3(c8[e & 3], sc(2 * e), sc(2 * e + 1));
+              c8[4 + (e & 3)] = max3(c8[4 + (e & 3)], sc(64 + 2 * e), sc(64 + 2 * e + 1));
+            }
+            tmem_st_32x32b_x32(tS, pk);
+            const float rmax = fmaxf(fmaxf(max3(c8[0], c8[1], c8[2]), max3(c8[3], c8[4], c8[5])), fmaxf(c8[6], c8[7]));
+            const float mbs = (rmax == -INFINITY) ? -INFINITY : rmax * p.scale_log2;
+            ATRACE(tr, 1, t, j);
+            if (!__any_sync(0xffffffffu, mbs > m + 8.f)) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                exp_pair(1, e);
+                if (e == CY_ATTN_PH_E) {  // group 0's P has long been stored: publish the first half
+                  tmem_st_wait();
+                  tc_fence_before();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(bPHalf + 8 * t);
+                }
+              }
+              tmem_st_32x32b_x32(tS + 32, pk);
+              ATRACE(tr, 2, t, j);
+              pp_pass(j);
+              tmem_st_wait();
+              l = l + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) +
+                       ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));  // (= l * corr + ..., corr = 1)
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bPReady + 8 * t);
+              ATRACE(tr, 3, t, j);
+              continue;
+            }
+            mx8[0] = rmax;
+            have_max = true;
+          }
+        }
+        // balanced 3-ary tree (depth 5, every level independent ops) instead of 8 serial chains
         float l1[43];
 #pragma unroll
         for (int i = 0; i < 42; ++i) l1[i] = max3(sc(3 * i), sc(3 * i + 1), sc(3 * i + 2));
@@ -657,7 +729,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
         float l3[5];
 #pragma unroll
         for (int i = 0; i < 5; ++i) l3[i] = max3(l2[3 * i], l2[3 * i + 1], l2[3 * i + 2]);
-        mx8[0] = max3(max3(l3[0], l3[1], l3[2]), l3[3], l3[4]);
+        if (!have_max) mx8[0] = max3(max3(l3[0], l3[1], l3[2]), l3[3], l3[4]);
       } else {
 #pragma unroll
         for (int g = 0; g < 2; ++g) {

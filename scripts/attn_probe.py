@@ -2,6 +2,9 @@
 import sys, os
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch
+from paper_2504_07004_b200 import _lib
+if os.environ.get("CY_EXP_LIB"):  # A/B against an experiment build
+    _lib.use_library(os.path.abspath(os.environ["CY_EXP_LIB"]))
 import paper_2504_07004_b200 as cy
 
 def bench(fn, iters=30):

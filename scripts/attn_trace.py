@@ -41,6 +41,8 @@ for t in range(2):
           f"exp_done->P_ready {d(2, 3, t):.0f} | P_ready->mma_Pfull {d(3, 5, t):.0f} | mma_Pfull->S_issued(j+1) {d(5, 6, t, shift=1):.0f} | "
           f"S_issued(j+1)->S_full(j+1) {st.median(T[0][t][j + 1] - T[6][t][j + 1] for j in range(8, 56)):.0f}")
 
+for t in range(2):
+    print(f"tile {t}: S_full -> TMEM loads done {d(0, 11, t):.0f} | loads done -> max_done {d(11, 1, t):.0f}")
 print("producer / MMA operand waits (cycles, j = 8..55 median):")
 kf = st.median(T[10][0][j] - T[8][0][j] for j in range(8, 56))
 vf = st.median(T[7][0][j] - T[9][0][j] for j in range(8, 56))
