@@ -9,7 +9,13 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sector_hit_rate.pct", "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
         "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "sm__ops_path_tensor_src_fp16_dst_fp32.sum",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        # L2 (LTS) load: throughput against its peak and sectors moved (the L2 -> SM feed of the narrow
+        # and batched tiles)
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors.sum", "lts__t_sectors_op_read.sum",
+        "lts__t_sectors_op_write.sum", "lts__cycles_elapsed.avg.per_second",
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
 out = {}
 for arg in sys.argv[1:]:
     name, path = arg.split("=", 1)

@@ -2,7 +2,7 @@
 # bench workload, the ncu launch list of the headline bench and one ncu --set full capture per
 # dominant kernel.  Outputs land in gpurun_out/ (copy the summaries into profiles/).
 set -u
-R=${ROUND:-r02}
+R=${ROUND:-r02d}
 mkdir -p gpurun_out/$R
 O=gpurun_out/$R
 timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest_exit=$?"; tail -2 $O/pytest_gpu.log
