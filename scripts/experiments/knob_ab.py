@@ -47,11 +47,13 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
             r = timeit(lambda i: cy.gemm_batched(sets[i % ns][0], sets[i % ns][1], sets[i % ns][2], 1.0, beta, out=D),
                        200, 2.0 * L * 1024 ** 3)
         elif w.startswith("g"):
-            n = int(w[1:])
+            # gN: short (burst clock); gNs: 3000 launches (~2 s, power-capped clock)
+            sus = w.endswith("s")
+            n = int(w[1:].rstrip("s"))
             sets = [(rnd(n, n), rnd(n, n)) for _ in range(2)]
             D = torch.empty((n, n), device="cuda", dtype=h)
-            r = timeit(lambda i: cy.gemm(sets[i % 2][0], sets[i % 2][1], out=D), max(20, int(4e13 / n ** 3)),
-                       2.0 * n ** 3)
+            r = timeit(lambda i: cy.gemm(sets[i % 2][0], sets[i % 2][1], out=D),
+                       3000 if sus else max(20, int(4e13 / n ** 3)), 2.0 * n ** 3)
         elif w == "rr65536":
             A, B = rnd(65536, 8192), rnd(8192, 8192)
             D = torch.empty((65536, 8192), device="cuda", dtype=h)
