@@ -709,6 +709,23 @@ def test_attention_peaky_and_bf16(causal):
     _attn_check("bf16", 1, 3, Qb, Kb, Vb, causal=False)
 
 
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_late_max_jump(causal):
+    """The running max jumps late (key block 3) and only for some rows of a warp: rows 400..463 meet
+    keys 384..447 equal to 6 x their own query (a jump of ~30 in log2 units, far past the lazy bound:
+    the speculative pass's P would overflow fp16 and must be discarded and redone), rows 464..479
+    keys at 1.5 x (a small jump, inside the bound: the speculative P stands), the other rows see
+    plain keys.  Everything against the oracle within the R15 bound.  (Checked to catch a broken
+    redo: a build that keeps the speculative P, CY_ATTN_MUTANT_NOREDO, fails only this test.)"""
+    Q, K, V = _attn_inputs(1, 2, 640, 640, seed=261)
+    q = decode(Q, "f16")
+    k = decode(K, "f16")
+    k[:, 384:448] = 6.0 * q[:, 400:464]
+    k[:, 448:464] = 1.5 * q[:, 464:480]
+    K = oracle.encode("f16", k)
+    _attn_check("f16", 1, 2, Q, K, V, causal)
+
+
 def test_attention_closed_forms():
     d = 128
     _, K, V = _attn_inputs(1, 2, 1, 300, seed=253)
