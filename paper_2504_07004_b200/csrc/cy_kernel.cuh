@@ -95,6 +95,13 @@ __device__ unsigned long long g_gemm_etrace[8 * 8 * 8];
 namespace cy {
 
 constexpr int kDebug = CY_DEBUG_MODE;
+// Experiment paths switched by Params fields the host sets only in CY_TUNING_KNOBS builds (L2
+// prefetch of later batches, C-tile L2 prefetch, D-store L2 policy): compiled out of the product.
+#ifdef CY_TUNING_KNOBS
+constexpr bool kTuning = true;
+#else
+constexpr bool kTuning = false;
+#endif
 
 enum Variant : int { V_GEMM = 0, V_DUAL_PAIR = 1, V_DUAL_SUM = 2, V_ROWREDUCE = 3, V_DUAL_GLU = 4 };
 
@@ -461,7 +468,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         sched_request(i);
         int b, mb, nb, kb0, kb1;
         unit_coords(p, t, sidx, b, mb, nb, kb0, kb1);
-        if (p.pf_dist > 0 && crank == 0 && b + p.pf_dist < p.L) {
+        // (timing experiments only: measured slower at every distance)
+        if (kTuning && p.pf_dist > 0 && crank == 0 && b + p.pf_dist < p.L) {
           // this tile's slice of problem b + pf_dist's operands (16-B granules)
           const int per_b = p.m_blocks * p.n_blocks;
           const int r = t - b * per_b;
@@ -759,7 +767,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const int buf = (C::NUM_ACC_BUF == 2) ? (it & 1) : 0;
       const uint32_t bph = (C::NUM_ACC_BUF == 2) ? ((it >> 1) & 1) : (it & 1);
       const int row0 = mb * C::CT_M + row_off + 32 * q4;
-      if (p.has_c && p.c_pf && lane == 0) {  // C of every chunk this warp will read, into L2
+      if (kTuning && p.has_c && p.c_pf && lane == 0) {  // C of every chunk this warp will read, into L2 (neutral)
 #pragma unroll 1
         for (int q = cpf ? 1 : 0; q < NQ; ++q) tma_prefetch_3d(chunk_c(q), chunk_n0(nb, q), row0, b);
       }
@@ -823,7 +831,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         if (lane == 0 && !(kDebug & 4)) {  // (debug 4: timing experiment without the D stores)
           const int n0 = chunk_n0(nb, q);
           const uint32_t sb = sE + slot * C::EPI_BUF_BYTES;
-          if (p.d_policy) tma_store_3d_hint(chunk_d(q), sb, n0, row0, b, dpol);
+          if (kTuning && p.d_policy) tma_store_3d_hint(chunk_d(q), sb, n0, row0, b, dpol);  // (neutral)
           else tma_store_3d(chunk_d(q), sb, n0, row0, b);
           for (int j = 0; j < p.n_extra; ++j) tma_store_3d(&extra.m[j], sb, n0, row0, b);  // replicas
           bulk_commit();
