@@ -69,6 +69,10 @@ using namespace cy;
 #ifndef CY_ATTN_SPEC
 #define CY_ATTN_SPEC 1
 #endif
+// CY_ATTN_DB: the default path runs attn_db_kernel (64-key blocks, double-buffered S in TMEM)
+#ifndef CY_ATTN_DB
+#define CY_ATTN_DB 0
+#endif
 // CY_ATTN_TRACE (timing experiments only, never in the product build): clock64() stamps of one
 // CTA's per-block events, read back with cy_attn_trace()
 #ifdef CY_ATTN_TRACE
@@ -115,10 +119,11 @@ struct Params {
   int l2hint;        // 1: TMA loads carry an L2 evict_last hint; 0: no hint (requests can merge in L2)
 };
 
-template <int DT, bool B_MN>
+template <int DT, bool B_MN, int N = 128>
 __host__ __device__ constexpr uint32_t idesc() {
-  // f32 accumulate, a/b format, a K-major, b K-major (S) or MN-major (PV), N = 128, M = 128
-  return (1u << 4) | (uint32_t(DT) << 7) | (uint32_t(DT) << 10) | ((B_MN ? 1u : 0u) << 16) | (uint32_t(128 >> 3) << 17) |
+  // f32 accumulate, a/b format, a K-major, b K-major (S) or MN-major (PV), N (128; 64 for the 64-key
+  // S blocks of attn_db_kernel), M = 128
+  return (1u << 4) | (uint32_t(DT) << 7) | (uint32_t(DT) << 10) | ((B_MN ? 1u : 0u) << 16) | (uint32_t(N >> 3) << 17) |
          (uint32_t(128 >> 4) << 24);
 }
 
@@ -890,6 +895,301 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
 
 
 
+#if CY_ATTN_DB
+// ============================================================================ double-buffered S kernel
+// Experiment build only (CY_ATTN_DB=1): correct (all attention tests) but slower than the default
+// kernel -- 1116-1164 vs 1254-1289 TFLOP/s at 2x16x8192, 990 vs 1075 causal.
+// attn_db_kernel: the two-tile layout with 64-key blocks so that each tile's S can be
+// double-buffered in TMEM (S_t buffers u = 0, 1 at columns 64 (2t + u); O_t at 256 + 128 t).  S_t(j+2)
+// goes into the buffer P_t(j) leaves once PV_t(j) has read it, so the scores of block j+1 are already in
+// TMEM when the softmax of block j finishes: the per-tile chain S -> softmax -> PV -> S of the default
+// kernel (which keeps P_t in the only S_t buffer) becomes softmax -> softmax, and the two tiles' softmax
+// warpgroups run side by side instead of taking turns.  K / V: 64-key tiles (16 KB) in 4-slot rings.
+namespace db {
+constexpr int BK = 64;                       // keys per block
+constexpr int KVT = BK * D * 2;              // one K or V tile: 16 KB (two SW128 atoms of 64 rows, 8 KB apart)
+constexpr int KV_ATOM = BK * 128;            // 8 KB
+constexpr int NS = 4;                        // K and V ring slots
+constexpr int SQ = 0, SK = NT * TILE, SV = SK + NS * KVT, BAR = SV + NS * KVT;
+constexpr int SMEM_BYTES = 1024 + BAR + 256;
+static_assert(SMEM_BYTES <= 232448, "DB layout exceeds 227 KB");
+__device__ __forceinline__ int blocks(const Params& p, int row_end) {
+  const int kv_end = p.causal ? min(p.sk, row_end) : p.sk;
+  return (kv_end + BK - 1) / BK;
+}
+}  // namespace db
+
+template <int DT>
+__global__ void __launch_bounds__(384, 1)
+    attn_db_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                   const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sQ = base + db::SQ, sK = base + db::SK, sV = base + db::SV;
+  const uint32_t bar = base + db::BAR;
+  const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bar + 40, bVFull = bar + 72, bVEmpty = bar + 104,
+                 bSFull = bar + 136 /* [t][u] */, bPReady = bar + 168, bOReady = bar + 184, sTmemSlot = bar + 200;
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = p.causal ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;  // heavy causal CTAs first
+  const int hb = blockIdx.y;
+  const int q0 = qt * BQ * NT;
+  int nkv[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) nkv[t] = db::blocks(p, q0 + BQ * (t + 1));
+  const int nall = nkv[NT - 1];
+
+  if (warp == W_PROD && lane == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    prefetch_tmap(&tmO);
+    mbar_init(bQFull, 1);
+    for (int s = 0; s < db::NS; ++s) {
+      mbar_init(bKFull + 8 * s, 1);
+      mbar_init(bKEmpty + 8 * s, 1);
+      mbar_init(bVFull + 8 * s, 1);
+      mbar_init(bVEmpty + 8 * s, 1);
+    }
+    for (int t = 0; t < NT; ++t) {
+      mbar_init(bSFull + 16 * t, 1);
+      mbar_init(bSFull + 16 * t + 8, 1);
+      mbar_init(bPReady + 8 * t, 4);
+      mbar_init(bOReady + 8 * t, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == W_MMA) {
+    tmem_alloc<1>(sTmemSlot, 512);
+    tmem_relinquish<1>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (warp >= 4 * NT) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    if (warp == W_PROD) {
+      // ---------------------------------------------------------------- producer
+      if (nall > 0) {
+        const uint64_t pol = policy_evict_last();
+        mbar_arrive_expect_tx_e(bQFull, NT * TILE);
+        for (int t = 0; t < NT; ++t) tma_load_4d_e(sQ + t * TILE, &tmQ, bQFull, 0, q0 + BQ * t, 0, hb, pol, true);
+        for (int j = 0; j < nall; ++j) {
+          const int s = j % db::NS;
+          const uint32_t ph = ((j / db::NS) & 1) ^ 1;
+          mbar_wait_w(bKEmpty + 8 * s, ph);
+          mbar_arrive_expect_tx_e(bKFull + 8 * s, db::KVT);
+          tma_load_4d_e(sK + s * db::KVT, &tmK, bKFull + 8 * s, 0, j * db::BK, 0, hb, pol, true);
+          mbar_wait_w(bVEmpty + 8 * s, ph);
+          mbar_arrive_expect_tx_e(bVFull + 8 * s, db::KVT);
+          tma_load_4d_e(sV + s * db::KVT, &tmV, bVFull + 8 * s, 0, j * db::BK, 0, hb, pol, true);
+        }
+      }
+    } else if (warp == W_MMA) {
+      // ---------------------------------------------------------------- MMA issuer
+      // S_t(j) -> buffer j & 1 (N = 64 keys); O_t += P_t(j) V_j with P_t(j) read from that buffer.
+      // Order: S(0), S(1) of both tiles, then per block j: PV_0(j), PV_1(j), S_0(j+2), S_1(j+2) --
+      // S_t(j+2) overwrites P_t(j) only after PV_t(j) (tcgen05 ops execute in order).
+      if (nall > 0) {
+        constexpr uint32_t ID_S = idesc<DT, false, 64>(), ID_PV = idesc<DT, true>();
+        auto issue_s = [&](int t, int j) {
+          const uint32_t ks = sK + (j % db::NS) * db::KVT;
+          const uint64_t kd0 = sdesc_sw128(ks, 16, 1024), qd0 = sdesc_sw128(sQ + t * TILE, 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t qoff = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+            const uint32_t koff = ((kk >> 2) * db::KV_ATOM + (kk & 3) * 32) >> 4;
+            mma_f16_e<1>(tmem + 64 * (2 * t + (j & 1)), qd0 + qoff, kd0 + koff, ID_S, kk > 0);
+          }
+          mma_commit_e<1>(bSFull + 16 * t + 8 * (j & 1), 0);
+        };
+        auto issue_pv = [&](int t, int j) {
+          const uint64_t vd0 = sdesc_sw128(sV + (j % db::NS) * db::KVT, db::KV_ATOM, 1024);
+          mbar_wait_w(bPReady + 8 * t, j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < db::BK / 16; ++kk)
+            mma_f16_ts_e(tmem + TM_O + t * 128, tmem + 64 * (2 * t + (j & 1)) + kk * 8, vd0 + kk * 128, ID_PV,
+                         (j | kk) != 0);
+          mma_commit_e<1>(bOReady + 8 * t, 0);
+        };
+        auto s_block = [&](int j) {  // S of both tiles for block j (K_j), then K_j's slot is free
+          const int s = j % db::NS;
+          mbar_wait_w(bKFull + 8 * s, (j / db::NS) & 1);
+          tc_fence_after();
+          for (int t = 0; t < NT; ++t)
+            if (j < nkv[t]) issue_s(t, j);
+          mma_commit_e<1>(bKEmpty + 8 * s, 0);
+        };
+        mbar_wait_w(bQFull, 0);
+        s_block(0);
+        if (nall > 1) s_block(1);
+        for (int j = 0; j < nall; ++j) {
+          const int s = j % db::NS;
+          mbar_wait_w(bVFull + 8 * s, (j / db::NS) & 1);
+          tc_fence_after();
+          for (int t = 0; t < NT; ++t)
+            if (j < nkv[t]) issue_pv(t, j);
+          mma_commit_e<1>(bVEmpty + 8 * s, 0);
+          if (j + 2 < nall) s_block(j + 2);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax / epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+    const int t = warp >> 2, q = warp & 3;
+    const int r = 32 * q + lane;
+    const int trow0 = q0 + BQ * t;
+    const int qrow = trow0 + r;
+    const int nk = nkv[t];
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const uint32_t tO = tmem + lane_base + TM_O + t * 128;
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    float m = -INFINITY, l = 0.f;
+    // PV_t(i) completes phase i of bOReady_t.  Once S_t(j) is complete so is PV_t(j-2) (issued before
+    // it), so at block j the barrier's current phase is j - 1 or j and a parity wait for phase j - 1
+    // is unambiguous; the softmax waits on it only before rescaling O, and once at the end.
+    for (int j = 0; j < nk; ++j) {
+      const uint32_t tS = tmem + lane_base + 64 * (2 * t + (j & 1));
+      mbar_wait(bSFull + 16 * t + 8 * (j & 1), (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[64];
+      tmem_ld_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      tmem_ld_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      tmem_ld_wait();
+      const int key0 = j * db::BK;
+      const bool full_block = (key0 + db::BK <= p.sk) && (!p.causal || key0 + db::BK - 1 <= trow0);
+      if (!full_block) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const int key = key0 + e;
+          if (key >= p.sk || (p.causal && key > qrow)) v[e] = __float_as_uint(-INFINITY);
+        }
+      }
+      auto sc = [&](int k) { return __uint_as_float(v[k]); };
+      auto max3 = [](float a, float b, float c) { return fmaxf(fmaxf(a, b), c); };
+      float2 sm4[4];
+      uint32_t pk[32];
+      // exponentials against `ms`, the row max reduced in 4 chains between them
+      float c4[4];
+      auto pass = [&](float ms, bool with_max) {
+        const float2 ms2 = make_float2(-ms, -ms);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float2 x = ffma2(make_float2(sc(2 * e), sc(2 * e + 1)), sc2, ms2);
+          float2 pe;
+          pe.x = ex2(x.x);
+          pe.y = ex2(x.y);
+          sm4[e & 3] = fadd2(sm4[e & 3], pe);
+          pk[e] = pack2<DT>(pe.x, pe.y);
+          if (with_max) c4[e & 3] = max3(c4[e & 3], sc(2 * e), sc(2 * e + 1));
+        }
+      };
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c4[u] = -INFINITY;
+      // speculative pass against the running max (the P of every block whose row max stays within
+      // the lazy bound); block 0 (m = -inf) always takes the path below
+      pass((m == -INFINITY) ? 0.f : m, true);
+      const float rmax = fmaxf(fmaxf(c4[0], c4[1]), fmaxf(c4[2], c4[3]));
+      const float mb = (rmax == -INFINITY) ? -INFINITY : rmax * p.scale_log2;
+      const bool grow = mb > m + 8.f;
+      float corr = 1.f;
+      if (__any_sync(0xffffffffu, grow)) {
+        float m_new = m;
+        if (grow) {
+          m_new = mb;
+          corr = ex2(m - m_new);  // 0 when m == -inf
+        }
+        if (j > 0) {
+          // O_t must hold PV_t(j-1) before it is rescaled (the only place the softmax touches O)
+          mbar_wait(bOReady + 8 * t, (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x32(tO + 32 * c, o);
+          }
+        }
+        m = m_new;
+        pass((m == -INFINITY) ? 0.f : m, false);
+      }
+      // Publishing P_t(j) (and storing it) only once PV_t(j-1) is complete is required: without this
+      // wait, sharp-softmax inputs (where other warps take the redo path) produced wrong P and sums
+      // in rows of warps that did not (measured, scripts/experiments/attn_nan.py); with it all 55
+      // attention tests pass.
+      if (j > 0) mbar_wait(bOReady + 8 * t, (j - 1) & 1);
+      tmem_st_32x32b_x32(tS, pk);  // P (16-bit pairs) over the block's first 32 score columns
+      tmem_st_wait();
+      l = l * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) + ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bPReady + 8 * t);
+    }
+    // ---------------------------------------------------------------- epilogue: O / l, lse
+    const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+    if (nk > 0) {
+      mbar_wait(bOReady + 8 * t, (nk - 1) & 1);
+      tc_fence_after();
+    }
+    const uint32_t sE = sQ + t * TILE + q * 4096;  // Q_t is no longer read (all S_t issued and done)
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t a0[32], a1[32];
+      if (nk > 0) {
+        tmem_ld_32x32b_x32(tO + 64 * c, a0);
+        tmem_ld_32x32b_x32(tO + 64 * c + 32, a1);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) a0[e] = a1[e] = 0u;
+      }
+      if (lane == 0 && c > 0) bulk_wait_read<0>();
+      __syncwarp();
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv) {
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int col = 8 * vv + 2 * u;
+          const float x0 = __uint_as_float(col < 32 ? a0[col] : a1[col - 32]) * inv_l;
+          const float x1 = __uint_as_float(col + 1 < 32 ? a0[col + 1] : a1[col + 1 - 32]) * inv_l;
+          w[u] = pack2<DT>(x0, x1);
+        }
+        st_shared_v4(sE + lane * 128 + ((vv ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&tmO, sE, 64 * c, trow0 + 32 * q, hb);
+        bulk_commit();
+      }
+    }
+    if (p.lse && qrow < p.sq)
+      p.lse[(size_t)hb * p.sq + qrow] = (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    if (lane == 0) bulk_wait_read<0>();
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, 512);
+  }
+}
+#endif  // CY_ATTN_DB
+
 #ifdef CY_ATTN_EXPERIMENTS  // measured slower than the default: experiment build only
 // ============================================================================ persistent two-tile kernel
 // The default layout (two 128-row query tiles per CTA, softmax warpgroup per tile, setmaxnreg)
@@ -1569,10 +1869,10 @@ bool g_attr_set[64][6][2][4] = {};
 int g_sms[64] = {};
 
 // {64 columns, rows, 2 column atoms, batch*head} with 128-row boxes of both atoms (one TMA op per tile)
-bool make_map4(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh) {
+bool make_map4(CUtensorMap* m, int dt, const void* ptr, uint64_t rows, uint64_t bh, uint32_t box_rows = 128) {
   cuuint64_t dims[4] = {64, rows, uint64_t(D) / 64, bh};
   cuuint64_t strides[3] = {uint64_t(D) * 2, 128, rows * uint64_t(D) * 2};
-  cuuint32_t box[4] = {64, 128, uint32_t(D) / 64, 1};
+  cuuint32_t box[4] = {64, box_rows, uint32_t(D) / 64, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return g_encode(m, dt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                   const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1659,10 +1959,11 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   const bool o32 = kern == 2 && split == 4;  // 32-column output boxes, unswizzled staging
   // the two-tile kernels (kern 1) load Q / K / V tiles as one 4-D box each; the pair kernel keeps 3-D maps
   const bool four = (kern == 1);
+  const uint32_t kv_rows = CY_ATTN_DB ? 64 : 128;  // K / V box rows (keys per block)
   bool ok = (four ? make_map4(&tQ, dt, Q, seq_q, bh) : make_map(&tQ, dt, Q, seq_q, bh, 64, 128)) &&
             make_map(&tO, dt, O, seq_q, bh, o32 ? 32 : 64, 32, !o32);
   if (seq_k > 0)
-    ok = ok && (four ? make_map4(&tK, dt, K, seq_k, bh) && make_map4(&tV, dt, V, seq_k, bh)
+    ok = ok && (four ? make_map4(&tK, dt, K, seq_k, bh, kv_rows) && make_map4(&tV, dt, V, seq_k, bh, kv_rows)
                      : make_map(&tK, dt, K, seq_k, bh, 64, kern == 2 ? 64 : 128) && make_map(&tV, dt, V, seq_k, bh, 64, 128));
   if (!ok) return CY_ERR_LAUNCH;
   Params p;
@@ -1733,12 +2034,20 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.l2hint = 1;  // evict_last on Q/K/V (measured: without it causal 16384 loses 6 %)
   constexpr int ki = 4, ei = 0;
   const int cs = 3;
+#if CY_ATTN_DB
+  const void* fn = dt == CY_F16 ? (const void*)&attn_db_kernel<0> : (const void*)&attn_db_kernel<1>;
+#else
   const void* fn = dt == CY_F16 ? (const void*)&attn_fwd_kernel<0, 0, 3> : (const void*)&attn_fwd_kernel<1, 0, 3>;
+#endif
 #endif
 #ifdef CY_ATTN_EXPERIMENTS
   const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : (kern == 1 && cs == 3) ? SMEM_BYTES3 : SMEM_BYTES;
 #else
+#if CY_ATTN_DB
+  const int smem = db::SMEM_BYTES;
+#else
   const int smem = SMEM_BYTES3;
+#endif
 #endif
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
