@@ -38,6 +38,11 @@
 #ifndef CY_DEBUG_MODE
 #define CY_DEBUG_MODE 0
 #endif
+// CY_C_FIRST: beta != 0 with one staging slot per epilogue warp: fetch the tile's first C chunk while
+// the main loop runs
+#ifndef CY_C_FIRST
+#define CY_C_FIRST 1
+#endif
 
 // CY_GEMM_TRACE (timing experiments only, never in the product build): clock64() stamps of one
 // CTA's per-tile events (scripts/gemm_trace.py reads them with cy_gemm_trace_read()).
@@ -759,6 +764,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     int t;
     // C prefetch: not with split-K (each split stores only some of its chunks)
     const bool cpf = CPF && p.has_c && SPL == 1;
+    // single staging slot (EPI_BUFS == 1): only the tile's first C chunk is fetched ahead (during the
+    // main loop); the others follow one at a time as the slot frees
+    const bool cpf0 = !CPF && p.has_c && SPL == 1 && CY_C_FIRST;
     uint32_t red_phase = 0;  // split-K: parity of this warp's bRed barrier
     for (int it = 0; sched_next(it, t, true); ++it) {
       int b, mb, nb, kb0, kb1;
@@ -771,7 +779,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll 1
         for (int q = cpf ? 1 : 0; q < NQ; ++q) tma_prefetch_3d(chunk_c(q), chunk_n0(nb, q), row0, b);
       }
-      if (cpf) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
+      if (cpf || cpf0) fetch_c(nb, row0, b, 0, slot);  // overlaps the tile's main loop
       if (ew == 0 && lane == 0) CY_TR(it, 8);
       if (p.sleep_ns) mbar_wait_sleep(bTFull + 8 * buf, bph, p.sleep_ns);
       else mbar_wait(bTFull + 8 * buf, bph);
@@ -815,7 +823,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         } add{w0, it, ew, lane};
 #endif
         if (p.has_c) {
-          if (!cpf) fetch_c(nb, row0, b, q, slot);
+          if (!cpf && !(cpf0 && q == 0)) fetch_c(nb, row0, b, q, slot);
           mbar_wait(cbar, cphase);
           cphase ^= 1;
         } else {
