@@ -334,7 +334,11 @@ double cfg_cost(int cg, int bn, int single_buf, int64_t m, int64_t n, int64_t k,
   // bandwidth) and reads back the same volume for its share of the reduction; one k-block costs
   // 2 bn cycles per SM, so the reduction weighs ~8 k-blocks = 512 K elements
   if (splits > 1) kk += 512.0;
-  return static_cast<double>(waves) * static_cast<double>(bm * bn) / cg * kk / eff;
+  // the last wave's epilogue is exposed whatever the buffering: draining 128 rows x bn columns per
+  // SM costs about bn / 2 k-equivalents (calibrated on batched 8 x 1024^3, where one wave of 256 x 512
+  // tiles measured 19.4 us against 18.1 us for two waves of 256 x 256; negligible for many waves)
+  const double tail = 0.5 * bn;
+  return (static_cast<double>(waves) * kk + tail) * static_cast<double>(bm * bn) / cg / eff;
 }
 
 // Menu entry and split count: the smallest predicted time.  max_splits > 1 lets split-K (V_GEMM
