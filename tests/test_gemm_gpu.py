@@ -352,6 +352,17 @@ def test_full_8192_sampled():
     assert_within_tol(D[rows], ref, n, "f16", what="8192^3 sampled")
 
 
+def test_full_16384_sampled():
+    """The largest square of the configs[1] sweep (bench sweep-16384), oracle on the first and last
+    row of every 256-row block plus random rows."""
+    n = 16384
+    A, B, _ = synth.gemm_inputs(n, n, n, seed=synth.seed_for(1, 1))
+    D = run_gemm(A, B, None, 1.0, 0.0, "f16")
+    rows = synth.sample_rows(n, tile=256, n_random=16)
+    ref = oracle.gemm("f16", A, B, rows=rows)
+    assert_within_tol(D[rows], ref, n, "f16", what="16384^3 sampled")
+
+
 def test_full_rowreduce_65536_sampled():
     """BASELINE configs[4] (65536 x 8192 x 8192, fused row reduction) as one single-GPU launch,
     oracle on sampled rows."""
