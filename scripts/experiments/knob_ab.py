@@ -1,6 +1,7 @@
 """A/B of the library's environment tuning knobs (read once at load, so one process per setting).
-    python scripts/experiments/knob_ab.py REPS WORKLOADS 'CY_PF=0' 'CY_PF=8' 'CY_PF=8 CY_SERP=1' ...
-WORKLOADS: comma list of batched, batched1 (beta=1), batched16 (L2-resident 16 x 1024^3), g8192, rr65536, g4096, g16384.
+    python scripts/experiments/knob_ab.py REPS WORKLOADS 'CY_GROUP_M=4' 'CY_GROUP_M=6 CY_SERP=0' 'CY_KNOBS_LIB=other.so' ...
+WORKLOADS: comma list of batched, batched1 (beta=1), batched16 (L2-resident 16 x 1024^3), gN (N^3, short), gNs
+(N^3, 3000 launches), rr65536.
 Settings run interleaved, REPS rounds, on build/exp/libcypress_knobs.so
 (scripts/build_experiment.py knobs CY_TUNING_KNOBS=1); prints us/launch and TFLOP/s per (setting, workload)."""
 import os
