@@ -73,6 +73,10 @@ using namespace cy;
 #ifndef CY_ATTN_DB
 #define CY_ATTN_DB 0
 #endif
+// CY_ATTN_T1: the default path runs attn_t1_kernel (one query tile per CTA, double-buffered S)
+#ifndef CY_ATTN_T1
+#define CY_ATTN_T1 0
+#endif
 // CY_ATTN_LPT: causal grids ordered heads-fastest, so the launch order is heaviest-first across the
 // whole grid (every head's last query tiles, then the next ones ...) and the tail of the launch holds
 // only the lightest CTAs.  Measured (scripts/attn_probe.py, two runs): causal 2x16x8192 1063 -> 1110
@@ -1200,6 +1204,274 @@ __global__ void __launch_bounds__(384, 1)
 }
 #endif  // CY_ATTN_DB
 
+#if CY_ATTN_T1
+// ============================================================================ one-tile kernel
+// Experiment build only (CY_ATTN_T1=1).  attn_t1_kernel: one 128-row query tile per CTA with S
+// double-buffered in TMEM (S buffers at columns 0 / 128, O at 256) and 8 softmax warps, two per TMEM
+// lane quarter, each taking 64 of the block's 128 keys (and 64 of O's columns).  The MMA order is
+// S(0), S(1), then per block PV(j), S(j+2): the scores of block j+1 are in TMEM while block j's softmax
+// runs, so consecutive blocks' softmax passes follow each other with no wait for the tensor core.
+namespace t1 {
+constexpr int NK = 3, NV = 3;                              // K and V ring slots (32 KB tiles)
+constexpr int SQ = 0, SK = TILE, SV = SK + NK * TILE, BAR = SV + NV * TILE;
+constexpr int XCH = BAR + 256;                             // [2 halves][128 rows] fp32 exchange
+constexpr int SMEM_BYTES = 1024 + XCH + 2 * 128 * 4;
+static_assert(SMEM_BYTES <= 232448, "T1 layout exceeds 227 KB");
+}  // namespace t1
+
+template <int DT>
+__global__ void __launch_bounds__(384, 1)
+    attn_t1_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                   const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sQ = base + t1::SQ, sK = base + t1::SK, sV = base + t1::SV;
+  const uint32_t bar = base + t1::BAR;
+  const uint32_t bQFull = bar, bKFull = bar + 8, bKEmpty = bar + 32, bVFull = bar + 56, bVEmpty = bar + 80,
+                 bSFull = bar + 104 /* [2] */, bPReady = bar + 120, bOReady = bar + 128, sTmemSlot = bar + 136;
+  float* xch = reinterpret_cast<float*>(smem_raw + (base + t1::XCH - raw));  // [2][128]
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (sTmemSlot - raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = p.lpt ? (gridDim.y - 1 - blockIdx.y) : p.causal ? (gridDim.x - 1 - blockIdx.x) : blockIdx.x;
+  const int hb = p.lpt ? blockIdx.x : blockIdx.y;
+  const int q0 = qt * BQ;
+  const int nk = blocks_for(p, q0 + BQ);
+
+  if (warp == W_PROD && lane == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    prefetch_tmap(&tmO);
+    mbar_init(bQFull, 1);
+    for (int s = 0; s < t1::NK; ++s) {
+      mbar_init(bKFull + 8 * s, 1);
+      mbar_init(bKEmpty + 8 * s, 1);
+    }
+    for (int s = 0; s < t1::NV; ++s) {
+      mbar_init(bVFull + 8 * s, 1);
+      mbar_init(bVEmpty + 8 * s, 1);
+    }
+    mbar_init(bSFull, 1);
+    mbar_init(bSFull + 8, 1);
+    mbar_init(bPReady, 8);
+    mbar_init(bOReady, 1);
+    fence_mbar_init();
+  }
+  if (warp == W_MMA) {
+    tmem_alloc<1>(sTmemSlot, 512);
+    tmem_relinquish<1>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    if (warp == W_PROD) {
+      if (nk > 0) {
+        const uint64_t pol = policy_evict_last();
+        mbar_arrive_expect_tx_e(bQFull, TILE);
+        tma_load_4d_e(sQ, &tmQ, bQFull, 0, q0, 0, hb, pol, true);
+        for (int j = 0; j < nk; ++j) {
+          const int ks = j % t1::NK, vs = j % t1::NV;
+          mbar_wait_w(bKEmpty + 8 * ks, ((j / t1::NK) & 1) ^ 1);
+#ifdef CY_ATTN_T1_NOLOAD  // timing experiment only (invalid results): no K / V reloads after the ring fill
+          if (j >= 3) {
+            mbar_arrive_e(bKFull + 8 * ks);
+            mbar_wait_w(bVEmpty + 8 * vs, ((j / t1::NV) & 1) ^ 1);
+            mbar_arrive_e(bVFull + 8 * vs);
+            continue;
+          }
+#endif
+          mbar_arrive_expect_tx_e(bKFull + 8 * ks, TILE);
+          tma_load_4d_e(sK + ks * TILE, &tmK, bKFull + 8 * ks, 0, j * BKV, 0, hb, pol, true);
+          mbar_wait_w(bVEmpty + 8 * vs, ((j / t1::NV) & 1) ^ 1);
+          mbar_arrive_expect_tx_e(bVFull + 8 * vs, TILE);
+          tma_load_4d_e(sV + vs * TILE, &tmV, bVFull + 8 * vs, 0, j * BKV, 0, hb, pol, true);
+        }
+      }
+    } else if (warp == W_MMA) {
+      if (nk > 0) {
+        constexpr uint32_t ID_S = idesc<DT, false>(), ID_PV = idesc<DT, true>();
+        auto issue_s = [&](int j) {
+          const int ks = j % t1::NK;
+          mbar_wait_w(bKFull + 8 * ks, (j / t1::NK) & 1);
+          tc_fence_after();
+          const uint64_t kd0 = sdesc_sw128(sK + ks * TILE, 16, 1024), qd0 = sdesc_sw128(sQ, 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+            mma_f16_e<1>(tmem + 128 * (j & 1), qd0 + off, kd0 + off, ID_S, kk > 0);
+          }
+          mma_commit_e<1>(bSFull + 8 * (j & 1), 0);
+          mma_commit_e<1>(bKEmpty + 8 * ks, 0);
+        };
+        mbar_wait_w(bQFull, 0);
+        tc_fence_after();
+        issue_s(0);
+        if (nk > 1) issue_s(1);
+        for (int j = 0; j < nk; ++j) {
+          const int vs = j % t1::NV;
+          mbar_wait_w(bVFull + 8 * vs, (j / t1::NV) & 1);
+          mbar_wait_w(bPReady, j & 1);
+          tc_fence_after();
+          const uint64_t vd0 = sdesc_sw128(sV + vs * TILE, ATOM, 1024);
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_f16_ts_e(tmem + TM_O, tmem + 128 * (j & 1) + kk * 8, vd0 + kk * 128, ID_PV, (j | kk) != 0);
+          mma_commit_e<1>(bOReady, 0);
+          mma_commit_e<1>(bVEmpty + 8 * vs, 0);
+          if (j + 2 < nk) issue_s(j + 2);  // into buffer j & 1, after PV(j) has read P(j) from it
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax / epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+    const int q = warp & 3, h = warp >> 2;  // lane quarter, key half (and O column half)
+    const int r = 32 * q + lane;
+    const int qrow = q0 + r;
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const uint32_t tO = tmem + lane_base + TM_O + 64 * h;
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    const uint32_t pair_bar = 1 + q;  // named barrier of the two warps of lane quarter q
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nk; ++j) {
+      const uint32_t tS = tmem + lane_base + 128 * (j & 1) + 64 * h;
+      mbar_wait(bSFull + 8 * (j & 1), (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[64];
+      tmem_ld_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      tmem_ld_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      tmem_ld_wait();
+      const int key0 = j * BKV + 64 * h;
+      const bool full_block = (j * BKV + BKV <= p.sk) && (!p.causal || j * BKV + BKV - 1 <= q0);
+      if (!full_block) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const int key = key0 + e;
+          if (key >= p.sk || (p.causal && key > qrow)) v[e] = __float_as_uint(-INFINITY);
+        }
+      }
+      auto sc = [&](int k) { return __uint_as_float(v[k]); };
+      auto max3 = [](float a, float b, float c) { return fmaxf(fmaxf(a, b), c); };
+      float2 sm4[4];
+      uint32_t pk[32];
+      float c4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c4[u] = -INFINITY;
+      auto pass = [&](float ms, bool with_max) {
+        const float2 ms2 = make_float2(-ms, -ms);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm4[u] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float2 x = ffma2(make_float2(sc(2 * e), sc(2 * e + 1)), sc2, ms2);
+          float2 pe;
+          pe.x = ex2(x.x);
+          pe.y = ex2(x.y);
+          sm4[e & 3] = fadd2(sm4[e & 3], pe);
+          pk[e] = pack2<DT>(pe.x, pe.y);
+          if (with_max) c4[e & 3] = max3(c4[e & 3], sc(2 * e), sc(2 * e + 1));
+        }
+      };
+      pass((m == -INFINITY) ? 0.f : m, true);
+      // the row's max over both halves: exchange with the partner warp of this lane quarter
+      const float hmax = fmaxf(fmaxf(c4[0], c4[1]), fmaxf(c4[2], c4[3]));
+      float* xm = xch + (j & 1) * 0;  // (one slot per half; the pair barrier below orders reuse)
+      xm[h * 128 + r] = hmax;
+      pair_sync();
+      const float rmax = fmaxf(hmax, xm[(h ^ 1) * 128 + r]);
+      pair_sync();  // both have read before the next block overwrites
+      const float mb = (rmax == -INFINITY) ? -INFINITY : rmax * p.scale_log2;
+      const bool grow = mb > m + 8.f;
+      float corr = 1.f;
+      // P(j) is stored and published only once PV(j-1) is complete (see attn_db_kernel)
+      if (j > 0) mbar_wait(bOReady, (j - 1) & 1);
+      if (__any_sync(0xffffffffu, grow)) {
+        float m_new = m;
+        if (grow) {
+          m_new = mb;
+          corr = ex2(m - m_new);
+        }
+        if (j > 0) {
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x32(tO + 32 * c, o);
+          }
+        }
+        m = m_new;
+        pass((m == -INFINITY) ? 0.f : m, false);
+      }
+      tmem_st_32x32b_x32(tmem + lane_base + 128 * (j & 1) + 32 * h, pk);  // P cols [32h, 32h + 32)
+      tmem_st_wait();
+      l = l * corr + (((sm4[0].x + sm4[0].y) + (sm4[1].x + sm4[1].y)) + ((sm4[2].x + sm4[2].y) + (sm4[3].x + sm4[3].y)));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bPReady);
+    }
+    // ---------------------------------------------------------------- epilogue: O / l, lse
+    xch[h * 128 + r] = l;
+    pair_sync();
+    const float lt = l + xch[(h ^ 1) * 128 + r];
+    const float inv_l = (lt > 0.f) ? 1.f / lt : 0.f;
+    if (nk > 0) {
+      mbar_wait(bOReady, (nk - 1) & 1);
+      tc_fence_after();
+    }
+    const uint32_t sE = sQ + warp * 4096;  // Q is no longer read: 4 KB staging per warp
+    uint32_t a0[32], a1[32];
+    if (nk > 0) {
+      tmem_ld_32x32b_x32(tO, a0);
+      tmem_ld_32x32b_x32(tO + 32, a1);
+      tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) a0[e] = a1[e] = 0u;
+    }
+#pragma unroll
+    for (int vv = 0; vv < 8; ++vv) {
+      uint32_t w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int col = 8 * vv + 2 * u;
+        const float x0 = __uint_as_float(col < 32 ? a0[col] : a1[col - 32]) * inv_l;
+        const float x1 = __uint_as_float(col + 1 < 32 ? a0[col + 1] : a1[col + 1 - 32]) * inv_l;
+        w[u] = pack2<DT>(x0, x1);
+      }
+      st_shared_v4(sE + lane * 128 + ((vv ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&tmO, sE, 64 * h, q0 + 32 * q, hb);
+      bulk_commit();
+    }
+    if (h == 0 && p.lse && qrow < p.sq)
+      p.lse[(size_t)hb * p.sq + qrow] = (lt > 0.f) ? (m + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
+    if (lane == 0) bulk_wait_read<0>();
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, 512);
+  }
+}
+#endif  // CY_ATTN_T1
+
 #ifdef CY_ATTN_EXPERIMENTS  // measured slower than the default: experiment build only
 // ============================================================================ persistent two-tile kernel
 // The default layout (two 128-row query tiles per CTA, softmax warpgroup per tile, setmaxnreg)
@@ -2045,7 +2317,9 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.l2hint = 1;  // evict_last on Q/K/V (measured: without it causal 16384 loses 6 %)
   constexpr int ki = 4, ei = 0;
   const int cs = 3;
-#if CY_ATTN_DB
+#if CY_ATTN_T1
+  const void* fn = dt == CY_F16 ? (const void*)&attn_t1_kernel<0> : (const void*)&attn_t1_kernel<1>;
+#elif CY_ATTN_DB
   const void* fn = dt == CY_F16 ? (const void*)&attn_db_kernel<0> : (const void*)&attn_db_kernel<1>;
 #else
   const void* fn = dt == CY_F16 ? (const void*)&attn_fwd_kernel<0, 0, 3> : (const void*)&attn_fwd_kernel<1, 0, 3>;
@@ -2054,7 +2328,9 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
 #ifdef CY_ATTN_EXPERIMENTS
   const int smem = kern == 2 ? pr::SMEM_BYTES : ps ? PS_SMEM_BYTES : (kern == 1 && cs == 3) ? SMEM_BYTES3 : SMEM_BYTES;
 #else
-#if CY_ATTN_DB
+#if CY_ATTN_T1
+  const int smem = t1::SMEM_BYTES;
+#elif CY_ATTN_DB
   const int smem = db::SMEM_BYTES;
 #else
   const int smem = SMEM_BYTES3;
@@ -2093,7 +2369,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   } else
 #endif
   {
-    const unsigned nq = (unsigned)((seq_q + BQ * NT - 1) / (BQ * NT));
+    const unsigned nq = (unsigned)((seq_q + BQ * (CY_ATTN_T1 ? 1 : NT) - 1) / (BQ * (CY_ATTN_T1 ? 1 : NT)));
     cfg.gridDim = p.lpt ? dim3((unsigned)bh, nq, 1) : dim3(nq, (unsigned)bh, 1);
     cfg.blockDim = dim3(cs == 3 ? 384 : THREADS, 1, 1);
     cfg.numAttrs = 1;
