@@ -50,11 +50,12 @@ def _dt(t):
 
 
 def _ld(t, name):
-    if t.dim() != 2:
+    st, sh = t.stride(), t.shape  # (two attribute reads: this runs for every operand of every call)
+    if len(st) != 2:
         raise ValueError(f"{name}: expected a 2-D tensor")
-    if t.stride(1) != 1 and t.size(1) > 1:
+    if st[1] != 1 and sh[1] > 1:
         raise ValueError(f"{name}: rows must be contiguous (row-major, stride(1) == 1)")
-    return t.stride(0) if t.size(0) > 1 else max(t.stride(0), t.size(1))
+    return st[0] if sh[0] > 1 else max(st[0], sh[1])
 
 
 def _empty2d(m, n, like):
