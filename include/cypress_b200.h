@@ -171,7 +171,8 @@ cy_status_t cy_gemm_rowreduce(cy_dtype_t dt, int64_t m, int64_t n, int64_t k, fl
  * Layout: Q [batch, heads, seq_q, 128], K and V [batch, heads, seq_k, 128], O like Q, all
  * contiguous (row stride 128 elements).  Scores and O accumulate in fp32 (TMEM); the softmax runs
  * in fp32 in the exp2 domain; P is rounded to the input type for the P.V product (as FA2/FA3 do).
- * lse may be NULL.  head_dim must be 128; batch*heads <= 65535.  O must not overlap Q, K, V. */
+ * lse may be NULL.  head_dim must be 128; batch*heads < 2^31 (above 65535 with ceil(seq_q / 256)
+ * <= 65535).  O must not overlap Q, K, V. */
 cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t heads, int64_t seq_q, int64_t seq_k,
                              int64_t head_dim, float scale, int causal, const void* Q, const void* K,
                              const void* V, void* O, float* lse, void* stream);

@@ -2191,7 +2191,10 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   const int64_t bh = batch * heads;
   if (bh == 0 || seq_q == 0) return CY_OK;
   if (!Q || !O || (seq_k > 0 && (!K || !V))) return CY_ERR_INVALID_VALUE;
-  if (seq_q > INT32_MAX || seq_k > INT32_MAX || bh > 65535) return CY_ERR_INVALID_VALUE;
+  // grid: (query-tile pairs, batch*heads), or (batch*heads, query-tile pairs) for causal problems and
+  // when batch*heads exceeds the 65535 limit of grid y
+  if (seq_q > INT32_MAX || seq_k > INT32_MAX || bh > INT32_MAX) return CY_ERR_INVALID_VALUE;
+  if (bh > 65535 && (seq_q + 2 * 128 - 1) / (2 * 128) > 65535) return CY_ERR_INVALID_VALUE;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al(Q) || !al(O) || (seq_k > 0 && (!al(K) || !al(V))) || (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)))
     return CY_ERR_MISALIGNED;
@@ -2255,7 +2258,7 @@ extern "C" cy_status_t cy_attention_fwd(cy_dtype_t dt, int64_t batch, int64_t he
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.lse = lse;
-  p.lpt = (causal && CY_ATTN_LPT && !CY_ATTN_DB) ? 1 : 0;
+  p.lpt = (((causal && CY_ATTN_LPT) || bh > 65535) && !CY_ATTN_DB && !CY_ATTN_T1) ? 1 : 0;
 #ifdef CY_ATTN_EXPERIMENTS
   // CY_ATTN_L2HINT: 1 = evict_last hint on the Q/K/V TMA loads, 0 = none (tuning knob)
   p.l2hint = [] {

@@ -753,6 +753,20 @@ def test_attention_closed_forms():
     assert_bits_equal(to_bits(O1).reshape(2, 7, d), np.repeat(V[:, :1], 7, axis=1), "one key")
 
 
+def test_attention_many_heads():
+    """batch*heads above the 65535 limit of a grid dimension (the launch puts heads on grid x): one key
+    per head, so O is that head's V row bit for bit and lse = 0 for zero queries."""
+    bh = 70000
+    d = 128
+    Q = torch.zeros((1, bh, 1, d), device="cuda", dtype=torch.float16)
+    K = torch.randn((1, bh, 1, d), device="cuda", dtype=torch.float16)
+    V = torch.randn((1, bh, 1, d), device="cuda", dtype=torch.float16)
+    O, lse = cy.attention(Q, K, V)
+    torch.cuda.synchronize()
+    assert torch.equal(O, V)
+    assert torch.equal(lse, torch.zeros_like(lse))
+
+
 # The attention variants that measured slower than the default are compiled only into an experiment
 # build (scripts/build_experiment.py attnexp CY_ATTN_EXPERIMENTS=1); run these with
 # CY_ATTN_EXPERIMENTS_LIB=build/exp/libcypress_attnexp.so (conftest loads that library instead).
