@@ -389,6 +389,19 @@ def test_ragged_multiwave_dynamic_schedule(cfg):
     assert_bits_equal(D[rows], oracle.encode("f16", oracle.gemm("f16", A, B, rows=rows)), f"cfg{cfg}")
 
 
+@pytest.mark.parametrize("cfg", ALL_CFGS)
+def test_ragged_multiwave_beta_c_every_tile(cfg):
+    """alpha/beta with C on a ragged multi-wave shape: every CTA runs several tiles, so the epilogue's
+    C staging (including the single-slot configs' first-chunk fetch during the next tile's main loop)
+    is reused across tiles; integer inputs, bit-exact on sampled rows and on the whole last row block."""
+    m, n, k = 4200, 3000, 200  # > 74 pair tiles even at 256 x 512
+    A, B, C = synth.gemm_inputs(m, n, k, seed=161 + cfg, kind="int", with_c=True)
+    D = run_gemm(A, B, C, 2.0, -1.0, "f16", cfg)
+    rows = np.unique(np.concatenate([synth.sample_rows(m, n_random=32), np.arange(m - 300, m)]))
+    want = oracle.encode("f16", oracle.gemm("f16", A, B, C, 2.0, -1.0, rows=rows))
+    assert_bits_equal(D[rows], want, f"cfg{cfg}")
+
+
 @pytest.mark.parametrize("mode", ["pair", "sum"])
 def test_dual_bf16(mode):
     m, n, k = 520, 392, 264
