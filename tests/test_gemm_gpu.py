@@ -402,6 +402,21 @@ def test_ragged_multiwave_beta_c_every_tile(cfg):
     assert_bits_equal(D[rows], want, f"cfg{cfg}")
 
 
+@pytest.mark.parametrize("cfg", [-1, 0, 1, 3])
+def test_dual_pair_multiwave_beta_integer(cfg):
+    """Dual PAIR with C0 / C1 on a ragged multi-wave shape (several tiles per CTA: C0 and C1 chunks
+    staged through the same slots tile after tile); integer inputs, bit-exact on sampled rows."""
+    m, n, k = 4200, 3000, 136
+    A, B0, B1, C0, C1 = synth.dual_inputs(m, n, k, seed=171 + cfg, kind="int", with_c=True)
+    cy.force_config(cfg)
+    d0, d1 = cy.dual_gemm(*(to_dev(x, "f16") for x in (A, B0, B1, C0, C1)), alpha=2.0, beta=-1.0, mode="pair")
+    torch.cuda.synchronize()
+    rows = synth.sample_rows(m, n_random=32)
+    r0, r1 = oracle.dual_gemm("f16", "pair", A, B0, B1, C0, C1, 2.0, -1.0, rows=rows)
+    assert_bits_equal(to_bits(d0)[rows], oracle.encode("f16", r0), f"D0 cfg{cfg}")
+    assert_bits_equal(to_bits(d1)[rows], oracle.encode("f16", r1), f"D1 cfg{cfg}")
+
+
 @pytest.mark.parametrize("mode", ["pair", "sum"])
 def test_dual_bf16(mode):
     m, n, k = 520, 392, 264
