@@ -267,6 +267,18 @@ def test_batched_64x1024_integer():
     assert_bits_equal(D[-1], want_last, "last batch")
 
 
+def test_batched_64x1024_beta_integer():
+    """The bench's batched-beta1 launch shape (64 x 1024^3 with C), integer inputs: bit-exact on the
+    first four batches and the last (the heuristic's 256 x 512 tiles, several per CTA)."""
+    L = 64
+    A, B, C = synth.gemm_inputs(1024, 1024, 1024, seed=103, batch=L, kind="int", with_c=True)
+    D = to_bits(cy.gemm_batched(to_dev(A, "f16"), to_dev(B, "f16"), to_dev(C, "f16"), 1.0, 1.0))
+    want = oracle.encode("f16", oracle.gemm_batched("f16", A[:4], B[:4], C[:4], 1.0, 1.0))
+    assert_bits_equal(D[:4], want, "batched beta=1 first 4")
+    want_last = oracle.encode("f16", oracle.gemm("f16", A[-1], B[-1], C[-1], 1.0, 1.0))
+    assert_bits_equal(D[-1], want_last, "batched beta=1 last batch")
+
+
 # ---------------------------------------------------------------- dual GEMM
 @pytest.mark.parametrize("cfg", [-1, 0, 1, 3])
 @pytest.mark.parametrize("shape", [(256, 256, 256), (333, 300, 190)])
