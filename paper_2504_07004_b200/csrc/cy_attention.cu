@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(CS == 3 ? 384 : THREADS, 1)
             const float rmax = fmaxf(fmaxf(max3(c8[0], c8[1], c8[2]), max3(c8[3], c8[4], c8[5])), fmaxf(c8[6], c8[7]));
             const float mbs = (rmax == -INFINITY) ? -INFINITY : rmax * p.scale_log2;
             ATRACE(tr, 1, t, j);
-#ifdef CY_ATTN_MUTANT_NOREDO  // test-the-test build only: keep the speculative P even when a row grows
+#if defined(CY_ATTN_MUTANT_NOREDO) || (defined(CY_MUTANT) && CY_MUTANT == 4)  // test-the-test builds only: keep the speculative P even when a row grows
             if (true) {
 #else
             if (!__any_sync(0xffffffffu, mbs > m + 8.f)) {

@@ -38,6 +38,14 @@
 #ifndef CY_DEBUG_MODE
 #define CY_DEBUG_MODE 0
 #endif
+// CY_MUTANT (scripts/mutants.sh only, never the product): one deliberate bug per value, to check
+// that the parity tests catch it -- 1 the epilogue drops beta*C on each warp's last chunk, 2 split-K
+// reduces one split too few, 3 the row reducers skip the last k-block, 4 (attention) the speculative
+// softmax keeps its P when a row's max grows, 5 the epilogue writes (and reads C) at the next
+// n-block's columns.
+#ifndef CY_MUTANT
+#define CY_MUTANT 0
+#endif
 // CY_C_FIRST: beta != 0 with one staging slot per epilogue warp: fetch the tile's first C chunk while
 // the main loop runs
 #ifndef CY_C_FIRST
@@ -748,6 +756,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     auto chunk_col = [&](int q) { return (C::EPI_SPLIT == 2 ? half : 0) + (q % CPW) * C::EPI_SPLIT; };
     // column of chunk q in the output; C/D maps of chunk q
     auto chunk_n0 = [&](int nb, int q) {
+      if (CY_MUTANT == 5 && p.n_blocks > 1) nb = (nb + 1) % p.n_blocks;  // (mutant: D to the wrong columns)
       return nb * C::CT_N + col_off + (C::DUAL ? 0 : (q / CPW) * C::BN) + 64 * chunk_col(q);
     };
     auto chunk_c = [&](int q) { return (C::VAR == V_DUAL_PAIR && q / CPW == 1) ? &tmC1 : &tmC0; };
@@ -877,6 +886,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 cf = unpack2<C::DT>(cv[e]);
+              if (CY_MUTANT == 1 && q == NQ - 1) continue;
               f[2 * e] = fmaf(p.beta, cf.x, f[2 * e]);
               f[2 * e + 1] = fmaf(p.beta, cf.y, f[2 * e + 1]);
             }
@@ -941,7 +951,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           for (int q = sidx; q < NQ; q += SPL) {
             uint32_t r[64];
 #pragma unroll 1
-            for (int s2 = 0; s2 < SPL; ++s2) {
+            for (int s2 = 0; s2 < SPL - (CY_MUTANT == 2 ? 1 : 0); ++s2) {
               const float4* src = wsl + size_t(s2) * SLICE4 + q * 16 * 32 + lane;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -1054,7 +1064,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       float acc = 0.f;
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         mbar_wait(bMDone + 8 * stage, phase);  // the tensor core has read this stage; it is still resident
-        if (do_red) {
+        if (do_red && !(CY_MUTANT == 3 && kb == p.k_blocks - 1)) {
 #pragma unroll
           for (int a = 0; a < C::KAT; ++a) {  // K-atoms in k order
             const uint32_t row_addr = sStage0 + stage * C::STAGE_BYTES + a * C::A_ATOM + r * 128;
