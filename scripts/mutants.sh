@@ -3,7 +3,8 @@
 # session).  Every line must end in "caught".  GPU box: bash scripts/mutants.sh
 set -u
 run() {  # mutant id, pytest -k expression
-  python scripts/build_experiment.py mutant$1 CY_MUTANT=$1 > /dev/null 2>&1 || { echo "mutant $1: build failed"; return; }
+  [ -f build/exp/libcypress_mutant$1.so ] || python scripts/build_experiment.py mutant$1 CY_MUTANT=$1 > /dev/null 2>&1 \
+    || { echo "mutant $1: build failed"; return; }
   out=$(CY_ATTN_EXPERIMENTS_LIB=build/exp/libcypress_mutant$1.so timeout 900 python -m pytest tests/test_gemm_gpu.py -m gpu -q -k "$2" 2>&1 | tail -1)
   case "$out" in *failed*) echo "mutant $1 ($2): caught -- $out";; *) echo "mutant $1 ($2): NOT caught -- $out";; esac
   rm -f build/exp/libcypress_mutant$1.so
